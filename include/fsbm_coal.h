@@ -1,0 +1,177 @@
+/* fsbm_coal.h -- C ABI of the B200-native FSBM collision-coalescence hot path.
+ *
+ * Drop-in boundary for the reference mini-app `coalbench`
+ * (/root/reference/proj).  Every entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; no exceptions cross the ABI: every
+ * function returns an fsbm_status and fsbm_last_error() holds the message.
+ *
+ * Data layout is the reference's GridState (driver.hpp:40-61): six separate
+ * category arrays bins[c][point*nkr + bin] with point = ((i-ids)*nk + (k-kds))*nj
+ * + (j-jds) (i slowest, j fastest, bin innermost); temperature/pressure are
+ * [npoints].  Category order liquid, ice1, ice2, ice3, snow, graupel
+ * (kernels.hpp:17-26).
+ */
+#ifndef FSBM_COAL_H
+#define FSBM_COAL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSBM_NCAT 6
+#define FSBM_ABI_VERSION 1
+
+/* Error taxonomy of errors.hpp:10-74 as status codes. */
+typedef enum {
+    FSBM_OK = 0,
+    FSBM_DOMAIN = 1,    /* DomainError    (errors.hpp:17-20) */
+    FSBM_SHAPE = 2,     /* ShapeError     (errors.hpp:23-26) */
+    FSBM_CONFIG = 3,    /* ConfigError    (errors.hpp:29-32) */
+    FSBM_STIFFNESS = 4, /* StiffnessError (errors.hpp:35-62) */
+    FSBM_ALLOC = 5,     /* AllocationError(errors.hpp:65-74) */
+    FSBM_CUDA = 6,      /* device/runtime failure (no reference analogue) */
+    FSBM_INTERNAL = 7
+} fsbm_status;
+
+/* coalbench::Ranges (driver.hpp:23-35): inclusive, 1-based as in WRF. */
+typedef struct {
+    int ids, ide, kds, kde, jds, jde;
+} fsbm_ranges;
+
+/* coalbench::ExecPlan (driver.hpp:103-109) + the numerics mode.
+ * mode: 0 serial, 1 parallel; collapse: 2 or 3; threads >= 1 (validated exactly
+ * as validate_plan, driver.cpp:213-221; the device ignores them -- scheduling
+ * never changes results); kernel_strategy: 0 precomputed, 1 on_demand (changes
+ * only the kernel_evals counter, kernels.cpp:154-172); scratch_strategy:
+ * 0 automatic, 1 arena.  numerics: FSBM_NUMERICS_FAST (FP64, reassociated
+ * sums; <=1e-12 relative per bin vs the reference) or FSBM_NUMERICS_EXACT
+ * (bitwise identical to coal_step: same operation order, no FMA). */
+enum { FSBM_PRECOMPUTED = 0, FSBM_ON_DEMAND = 1 };
+enum { FSBM_AUTOMATIC = 0, FSBM_ARENA = 1 };
+enum { FSBM_NUMERICS_FAST = 0, FSBM_NUMERICS_EXACT = 1 };
+typedef struct {
+    int mode;
+    int collapse;
+    int threads;
+    int kernel_strategy;
+    int scratch_strategy;
+    int numerics;
+} fsbm_plan;
+
+/* PatchTilePlan::Tile (driver.hpp:69-80), listed in patch-major, tile-minor
+ * order.  Only affects which point a StiffnessError reports (the first failing
+ * point in (tile, j, k, i) order, as run_chunks/fissioned_step would). */
+typedef struct {
+    int its, ite, jts, jte;
+} fsbm_tile;
+
+/* CoalCounters (coalescence.hpp:68-71) + KernelTableSet::eval_count
+ * (kernels.hpp:101-102): triples = (pair,i,j) visits, points = coal_step calls. */
+typedef struct {
+    uint64_t triples;
+    uint64_t points;
+    uint64_t kernel_evals;
+} fsbm_counters;
+
+/* StiffnessError (errors.hpp:35-62) incl. at_point (1-based i,k,j). */
+typedef struct {
+    int category, bin;
+    int has_point;
+    int i, k, j;
+} fsbm_error;
+
+typedef struct fsbm_ctx fsbm_ctx; /* opaque: device tables, gain table, registry */
+
+const char *fsbm_last_error(void);
+int fsbm_abi_version(void);
+
+/* Replaces the setup of StepContext{tables, gains} (driver.hpp:141-150):
+ * KernelTableSet (kernels.hpp:81-114, t750/t500 laid out [pair][i][j] as
+ * kernels.hpp:105-107), the registry (kernels.hpp:33-50; abd[3p..3p+2] =
+ * source_a, source_b, dest) and GainTable(grid) (coalescence.cpp:36-67, built
+ * here bit-identically from x[] and ratio, MassGrid mass_grid.hpp:9-14).
+ * Uploads everything to `device` once; no allocation happens per step. */
+int fsbm_ctx_create(int device, int nkr, const double *x, double ratio, int npairs,
+                    const int *pair_abd, const double *t750, const double *t500,
+                    fsbm_ctx **out);
+int fsbm_ctx_destroy(fsbm_ctx *ctx);
+
+/* GainTable::at(i,j) (coalescence.hpp:58) for the whole nkr x nkr table, as
+ * built by fsbm_ctx_create (flux-target selection; bit-exact contract). */
+int fsbm_ctx_gain_table(const fsbm_ctx *ctx, int32_t *lo, double *w_lo, double *w_hi,
+                        double *top);
+
+/* fission_predicates (driver.cpp:198-211) on device: mask[p] = T>193.15 &&
+ * T>223.15; *count = true_count.  stream may be NULL (legacy default stream). */
+int fsbm_fission_predicates_device(fsbm_ctx *ctx, size_t npoints, const double *temperature_d,
+                                   uint8_t *mask_d, uint64_t *count, void *stream);
+
+/* Phase 2 of fissioned_step (driver.cpp:353-434, driver.hpp:179-180) on
+ * DEVICE buffers: coal_step (coalescence.cpp:204-339) at exactly the mask-true
+ * points, in place.  temperature_d is used for the stale-mask check
+ * (driver.cpp:361-367) and may be NULL to skip it; mask_d may be NULL to derive
+ * it from temperature_d.  tiles may be NULL (whole domain).  counters_out (may
+ * be NULL) receives this call's counts; err_out (may be NULL) is filled on
+ * FSBM_STIFFNESS with the first failing point in (tile, j, k, i) order.  The
+ * call is stream-ordered but synchronises once at the end to report status.
+ * After FSBM_STIFFNESS the state is unspecified (the reference leaves it
+ * partially mutated too). */
+int fsbm_step_grid_device(fsbm_ctx *ctx, fsbm_ranges ranges, double *const bins_d[FSBM_NCAT],
+                          const double *pressure_d, const double *temperature_d,
+                          const uint8_t *mask_d, double dt, int substeps, const fsbm_plan *plan,
+                          const fsbm_tile *tiles, int ntiles, void *stream,
+                          fsbm_counters *counters_out, fsbm_error *err_out);
+
+/* Same on HOST buffers (the reference's GridState vectors): H2D of the state,
+ * the step, D2H of the bins -- pipelined in chunks over i-slabs so copies
+ * overlap compute.  Pinned host memory is fastest but not required. */
+int fsbm_step_grid_host(fsbm_ctx *ctx, fsbm_ranges ranges, double *const bins_h[FSBM_NCAT],
+                        const double *pressure_h, const double *temperature_h,
+                        const uint8_t *mask_h, double dt, int substeps, const fsbm_plan *plan,
+                        const fsbm_tile *tiles, int ntiles, fsbm_counters *counters_out,
+                        fsbm_error *err_out);
+
+/* coal_step (coalescence.hpp:148-150) for ONE point on host spans (bins6 is
+ * category-major [6][nkr]); a one-point launch.  Error semantics as coal_step
+ * (DomainError on dt<=0 / substeps<1). */
+int fsbm_coal_step(fsbm_ctx *ctx, double *bins6, double pressure, double dt, int substeps,
+                   int kernel_strategy, int numerics, fsbm_counters *counters_out,
+                   fsbm_error *err_out);
+
+/* ---- synthetic inputs (bench / parity fixtures; not part of the step) ---- */
+
+/* make_synthetic_case's temperature/pressure recipe (driver.cpp:223-272) on the
+ * host: exactly round(cf*N) cloudy points chosen by a SplitMix64 Fisher-Yates
+ * shuffle, cloudy T = 240+60u, others 210/180 K, pressure 900->400 hPa in k.
+ * liquid_init (nullable, [npoints*nkr]) receives the reference's liquid-only
+ * spectra (driver.cpp:274-283) for cloudy points. */
+int fsbm_synth_thermo_host(int ni, int nk, int nj, double cloud_fraction, uint64_t seed,
+                           int nkr, const double *x, double number_density,
+                           double *temperature, double *pressure, double *liquid_init);
+
+/* SURVEY 8(d) "thunderstorm" spectra for every mask-true point, generated on
+ * device (counter-based: SplitMix64(seed ^ (point_offset + p))); all six
+ * categories; mask-false points are zeroed.  point_offset is the global linear
+ * index of local point 0, so a shard reproduces its slice of the full domain. */
+int fsbm_synth_thunderstorm_device(fsbm_ctx *ctx, size_t npoints, uint64_t point_offset,
+                                   const uint8_t *mask_d, uint64_t seed,
+                                   double *const bins_d[FSBM_NCAT], void *stream);
+
+/* Device time (CUDA events on the launching stream) of the coalescence kernel in
+ * the most recent fsbm_step_grid_* call on this context, in milliseconds, and
+ * the number of this library's kernels that call launched. */
+int fsbm_ctx_last_timing(const fsbm_ctx *ctx, float *coal_kernel_ms, int *launches);
+
+/* Measured FP64 roof of `device`: a DFMA-chain microbenchmark (8 independent
+ * chains per thread, full occupancy) timed with CUDA events; FLOP/s counts 2 per
+ * DFMA.  MEASURED_PEAKS.json carries HBM and bf16 only, so the bench measures
+ * the denominator of its FP64 roofline live with this. */
+int fsbm_probe_fp64_peak(int device, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSBM_COAL_H */

@@ -298,6 +298,20 @@ int orc_thunderstorm_point(int nkr, const double *x, uint64_t seed, uint64_t p, 
     return ORC_OK;
 }
 
+int orc_thunderstorm_block(int nkr, const double *x, uint64_t seed, uint64_t p0, uint64_t n,
+                           const uint8_t *mask, double *bins) {
+    double *tmp = (double *)malloc(sizeof(double) * ORC_NCAT * nkr);
+    for (uint64_t q = 0; q < n; ++q) {
+        const int on = mask ? mask[q] != 0 : 1;
+        if (on && orc_thunderstorm_point(nkr, x, seed, p0 + q, tmp)) { free(tmp); return ORC_DOMAIN; }
+        for (int c = 0; c < ORC_NCAT; ++c)
+            for (int k = 0; k < nkr; ++k)
+                bins[(size_t)c * n * nkr + q * nkr + k] = on ? tmp[c * nkr + k] : 0.0;
+    }
+    free(tmp);
+    return ORC_OK;
+}
+
 uint64_t orc_fission_predicates(uint64_t npoints, const double *temperature, uint8_t *mask) {
     uint64_t count = 0; /* driver.cpp:198-211 */
     for (uint64_t p = 0; p < npoints; ++p) {

@@ -66,6 +66,11 @@ int orc_synthetic_case(int ni, int nk, int nj, double cloud_fraction, uint64_t s
  * SplitMix64(seed ^ p).  out: [6][nkr]. */
 int orc_thunderstorm_point(int nkr, const double *x, uint64_t seed, uint64_t p, double *out);
 
+/* orc_thunderstorm_point for points p0..p0+n-1 where mask (nullable) is set;
+ * others zeroed.  bins category-major [6][n*nkr]. */
+int orc_thunderstorm_block(int nkr, const double *x, uint64_t seed, uint64_t p0, uint64_t n,
+                           const uint8_t *mask, double *bins);
+
 /* proj/src/driver.cpp:198-211 */
 uint64_t orc_fission_predicates(uint64_t npoints, const double *temperature, uint8_t *mask);
 

@@ -72,6 +72,8 @@ class Oracle:
                                          C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp,
                                          _dp]
         L.orc_thunderstorm_point.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64, _dp]
+        L.orc_thunderstorm_block.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                             C.c_void_p, _dp]
         L.orc_fission_predicates.argtypes = [C.c_uint64, _dp, _u8p]
         L.orc_fission_predicates.restype = C.c_uint64
         L.orc_step_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _ip, _dp,
@@ -154,6 +156,15 @@ class Oracle:
         if st:
             raise ValueError(f"thunderstorm_point status {st}")
         return out.reshape(NCAT, len(x))
+
+    def thunderstorm_block(self, x, seed, p0, n, mask=None):
+        out = np.zeros(NCAT * n * len(x))
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        st = self.lib.orc_thunderstorm_block(len(x), x, seed, p0, n,
+                                             None if m is None else m.ctypes.data, out)
+        if st:
+            raise ValueError(f"thunderstorm_block status {st}")
+        return out.reshape(NCAT, n, len(x))
 
     def fission_predicates(self, T):
         mask = np.zeros(len(T), np.uint8)
