@@ -373,6 +373,7 @@ def run_ours(args):
                 "roofline": roof, "cpu_baseline": cpu,
                 "clocks": clk.summary(),
                 "diagnostics": {"updates_per_step": points, "triples_per_step": triples,
+                                "mass_before": m0g, "mass_after": m1g,
                                 "mass_rel_drift": abs(m1g - m0g) / m0g, "wall_s_timed": wall}}
         print(json.dumps(line), flush=True)
     if world > 1:

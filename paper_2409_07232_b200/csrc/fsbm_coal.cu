@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -22,6 +23,7 @@
 #include "../../include/fsbm_coal.h"
 #include "coal_exact.cuh"
 #include "coal_fast.cuh"
+#include "coal_dmma.cuh"
 #include "fsbm_common.cuh"
 
 using namespace fsbm;
@@ -77,6 +79,8 @@ struct fsbm_ctx {
     int32_t *d_glo = nullptr;
     double *d_gwlo = nullptr, *d_gwhi = nullptr, *d_gtop = nullptr;
     FastTables fast{};
+    DmmaTables dmma{};
+    int fast_kernel = 0; // 0 auto, 1 direct (coal_fast), 2 dmma (FSBM_FAST_KERNEL)
     // per-step workspace (grown on demand, never per-step allocated in steady state)
     void *d_ws = nullptr;
     size_t ws_bytes = 0;
@@ -147,6 +151,7 @@ void free_ctx(fsbm_ctx *c) {
     cudaFree(c->d_gwhi);
     cudaFree(c->d_gtop);
     free_fast_tables(c->fast);
+    free_dmma_tables(c->dmma);
     cudaFree(c->d_ws);
     cudaFree(c->d_arena);
     cudaFree(c->d_sink);
@@ -363,7 +368,13 @@ int step_device(fsbm_ctx *c, fsbm_ranges r, double *const bins[FSBM_NCAT], const
         coal_exact_kernel<<<blocks, kExactThreads, 0, s>>>(A, c->d_arena);
         FSBM_CUDA_TRY(cudaGetLastError());
     } else {
-        if (int st = launch_fast(c->fast, A, c->num_sms, s)) return fail(st, fast_last_error());
+        int st = -1;
+        if (c->fast_kernel != 1) st = launch_dmma(c->dmma, c->fast, A, c->num_sms, s);
+        if (st > 0) return fail(st, fast_last_error());
+        if (st < 0) {
+            if (c->fast_kernel == 2) return fail(FSBM_CONFIG, "FSBM_FAST_KERNEL=dmma unsupported for this nkr");
+            if (int st2 = launch_fast(c->fast, A, c->num_sms, s)) return fail(st2, fast_last_error());
+        }
     }
     FSBM_CUDA_TRY(cudaEventRecord(c->ev1, s));
     c->timed = true;
@@ -523,7 +534,11 @@ int fsbm_ctx_create(int device, int nkr, const double *x, double ratio, int npai
     if (!st) {
         st = build_fast_tables(c->fast, nkr, c->x, npairs, c->abd, t750, t500, c->g_lo, c->g_wlo,
                                c->g_whi, c->g_top);
+        if (!st) st = build_dmma_tables(c->dmma, nkr, npairs, c->abd, t750, t500, c->g_lo,
+                                        c->g_wlo, c->g_whi, c->g_top);
         if (st) fail(st, fast_last_error());
+        if (const char *ev = std::getenv("FSBM_FAST_KERNEL"))
+            c->fast_kernel = std::string(ev) == "direct" ? 1 : std::string(ev) == "dmma" ? 2 : 0;
     }
     if (st) {
         free_ctx(c);

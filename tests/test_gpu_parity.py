@@ -194,13 +194,14 @@ def test_custom_registry_aliasing(oracle):
     """Non-standard registry: a==dest cross pair, 3-category pair, repeated dest."""
     pairs = [fsbm.InteractionPair("gl", 5, 0, 5), fsbm.InteractionPair("sl", 4, 0, 5),
              fsbm.InteractionPair("ll", 0, 0, 0), fsbm.InteractionPair("il", 1, 0, 0)]
-    ctx, grid, tabs = make_ctx(33, pairs=pairs)
+    ctx, grid, tabs = make_ctx(33, pairs=pairs, coeff=0.1)
     st, mask, B = thunder_host(oracle, ctx, 3, 3, 4, 1.0, 9)
-    s, cnt_o, _, Bo = run_oracle_grid(oracle, ctx, tabs, st, mask, B)
+    s, cnt_o, _, Bo = run_oracle_grid(oracle, ctx, tabs, st, mask, B, dt=0.5)
     assert s == 0
     for numerics in ("exact", "fast"):
         st2 = fsbm.GridState(st.ranges, grid, st.temperature, st.pressure, [b.copy() for b in st.bins])
-        fsbm.fissioned_step(st2, None, fsbm.StepContext(ctx), fsbm.ExecPlan(numerics=numerics))
+        fsbm.fissioned_step(st2, None, fsbm.StepContext(ctx, fsbm.CoalConfig(0.5)),
+                            fsbm.ExecPlan(numerics=numerics))
         got = np.stack([b.reshape(-1, 33) for b in st2.bins])
         if numerics == "exact":
             assert np.array_equal(got, Bo)
