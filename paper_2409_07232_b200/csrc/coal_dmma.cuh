@@ -22,6 +22,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -33,6 +34,7 @@ namespace fsbm {
 
 struct DmmaTables {
     int nkr = 0, S = 0, npairs = 0;
+    int kf[2][8] = {}, km[2][8] = {}; // see DmmaArgs
     double *blob = nullptr;  // [pair][TR500 | TRd | TC500 | TCd], each [nkr][S], zero padded
     double *gains = nullptr; // [GRlo | GRhi | GClo | GChi], each [nkr][S]
 };
@@ -85,6 +87,29 @@ inline int build_dmma_tables(DmmaTables &D, int nkr, int npairs, const std::vect
                 gains[2 * nn + static_cast<size_t>(j) * S + i] = clo;
                 gains[3 * nn + static_cast<size_t>(j) * S + i] = chi;
             }
+        }
+    // K-step classification per pass / 8-row block (prefix structure of owned far cells)
+    const int KS = S / 4;
+    for (int X = 0; X < 2; ++X)
+        for (int b = 0; b < nkr / 8 && b < 8; ++b) {
+            const double *glo = gains.data() + (2 * X) * nn, *ghi = glo + nn;
+            auto cls = [&](int ks) { // 0 all far-owned (clo+chi==1), 2 all zero, 1 mixed
+                bool all_one = true, all_zero = true;
+                for (int r = 0; r < 8; ++r)
+                    for (int c = 0; c < 4; ++c) {
+                        const size_t ix = static_cast<size_t>(8 * b + r) * S + 4 * ks + c;
+                        const double sum = glo[ix] + ghi[ix];
+                        all_one = all_one && std::fabs(sum - 1.0) <= 4e-16;
+                        all_zero = all_zero && glo[ix] == 0.0 && ghi[ix] == 0.0;
+                    }
+                return all_one ? 0 : all_zero ? 2 : 1;
+            };
+            int kf = 0;
+            while (kf < KS && cls(kf) == 0) ++kf;
+            int km = KS;
+            while (km > kf && cls(km - 1) == 2) --km;
+            D.kf[X][b] = kf;
+            D.km[X][b] = km;
         }
     D.nkr = nkr;
     D.S = S;
@@ -141,6 +166,7 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 
 struct DmmaArgs {
     int S, RB, tail;      // padded stream length, full 8-row blocks, tail rows
+    int kf[2][8], km[2][8]; // per pass/block: leading all-owned-far K-steps, end of gain K-steps
     int QP;               // smem point pitch (>= NP, = 4 mod 16)
     uint32_t nbatches;
     const double *blob, *gains;
@@ -316,9 +342,20 @@ __global__ void __launch_bounds__(384, 1)
                             on[nt][e] = act[q] >> cur & 1ull;
                             we[nt][e] = wts[q];
                         }
-                    double wb[NT];
+                    // Pressure-weight mode of this warp's 16 points (warp-uniform):
+                    //   0: all w == 0 (p <= 500 hPa)  -> K500 + Kd*0 == K500 exactly: one half
+                    //   1: all w == 1 (p >= 750 hPa)  -> K = K500 + Kd (the same sum the
+                    //      reference forms): one half on the summed table
+                    //   2: otherwise                   -> K500 half + w * (Kd half)
+                    bool all0 = true, all1 = true;
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) wb[nt] = wts[qg + nt * 8 + lr];
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            all0 = all0 && we[nt][e] == 0.0;
+                            all1 = all1 && we[nt][e] == 1.0;
+                        }
+                    const int wmode = __all_sync(0xffffffffu, all0) ? 0 : __all_sync(0xffffffffu, all1) ? 1 : 2;
                     for (int X = 0; X < (self ? 1 : 2); ++X) {
                         const double *T5 = tb + (2 * X) * TBL;
                         const double *Td = T5 + TBL;
@@ -326,31 +363,71 @@ __global__ void __launch_bounds__(384, 1)
                         const double *Ghi = Glo + TBL;
                         const int vcat = X == 0 ? pb : pa; // stream category
                         const int fcat = X == 0 ? pa : pb; // owner scale / loss category
-                        double acc[3][NT][2];
+                        const int kf = F.kf[X][b], km = F.km[X][b], KS = S / 4;
+                        // Y1 = loss sum, Y2 = lo-gain sum, YG = sum of T*(clo+chi) v, so
+                        // Y3 (hi-gain) = YG - Y2.  In the leading K-steps every cell of the
+                        // block is an owned far cell (clo+chi == 1), so YG reuses the loss DMMAs
+                        // there; only the diagonal ("mixed") steps need an explicit T*(clo+chi).
+                        double Y1[NT][2], Y2[NT][2], YG[NT][2];
 #pragma unroll
-                        for (int k = 0; k < 3; ++k)
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) acc[k][nt][0] = acc[k][nt][1] = 0.0;
+                        for (int nt = 0; nt < NT; ++nt)
+                            Y1[nt][0] = Y1[nt][1] = Y2[nt][0] = Y2[nt][1] = YG[nt][0] = YG[nt][1] = 0.0;
                         const size_t arow = static_cast<size_t>(o0 + lr) * S + lc;
-#pragma unroll 1
-                        for (int half = 0; half < 2; ++half) {
-                            const double *Th = half ? Td : T5;
-#pragma unroll 3
-                            for (int ks = 0; ks < S / 4; ++ks) {
+                        const double *vb = &W(vcat, lc, qg + lr);
+                        const int nhalf = wmode == 2 ? 2 : 1;
+                        for (int h = 0; h < nhalf; ++h) {
+                            // h == 0: K500 (mode 0/2) or K500+Kd (mode 1); h == 1: Kd (mode 2)
+                            const double *Ta = (h == 0) ? T5 : Td;
+                            const bool summed = wmode == 1;
+                            double c1o[NT][2], c1r[NT][2], c2[NT][2], cg[NT][2];
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt)
+                                c1o[nt][0] = c1o[nt][1] = c1r[nt][0] = c1r[nt][1] = c2[nt][0] = c2[nt][1] =
+                                    cg[nt][0] = cg[nt][1] = 0.0;
+#pragma unroll 2
+                            for (int ks = 0; ks < kf; ++ks) { // owned far cells only
                                 const size_t ai = arow + 4 * ks;
-                                const double t = Th[ai];
-                                const double a2 = t * Glo[ai];
-                                const double a3 = t * Ghi[ai];
-                                const int s = 4 * ks + lc;
+                                const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+                                const double t2 = t * Glo[ai];
 #pragma unroll
                                 for (int nt = 0; nt < NT; ++nt) {
-                                    double v = W(vcat, s, qg + nt * 8 + lr);
-                                    if (half) v *= wb[nt];
-                                    dmma(acc[0][nt][0], acc[0][nt][1], t, v);
-                                    dmma(acc[1][nt][0], acc[1][nt][1], a2, v);
-                                    dmma(acc[2][nt][0], acc[2][nt][1], a3, v);
+                                    const double v = vb[static_cast<size_t>(4 * ks) * QP + nt * 8];
+                                    dmma(c1o[nt][0], c1o[nt][1], t, v);
+                                    dmma(c2[nt][0], c2[nt][1], t2, v);
                                 }
                             }
+                            for (int ks = kf; ks < km; ++ks) { // diagonal / mixed steps
+                                const size_t ai = arow + 4 * ks;
+                                const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+                                const double lo = Glo[ai];
+                                const double t2 = t * lo, tg = t * (lo + Ghi[ai]);
+#pragma unroll
+                                for (int nt = 0; nt < NT; ++nt) {
+                                    const double v = vb[static_cast<size_t>(4 * ks) * QP + nt * 8];
+                                    dmma(c1r[nt][0], c1r[nt][1], t, v);
+                                    dmma(c2[nt][0], c2[nt][1], t2, v);
+                                    dmma(cg[nt][0], cg[nt][1], tg, v);
+                                }
+                            }
+#pragma unroll 2
+                            for (int ks = km; ks < KS; ++ks) { // no gains owned by this pass
+                                const size_t ai = arow + 4 * ks;
+                                const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+#pragma unroll
+                                for (int nt = 0; nt < NT; ++nt) {
+                                    const double v = vb[static_cast<size_t>(4 * ks) * QP + nt * 8];
+                                    dmma(c1r[nt][0], c1r[nt][1], t, v);
+                                }
+                            }
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const double sc = h == 1 ? we[nt][e] : 1.0;
+                                    Y1[nt][e] = fma(sc, c1o[nt][e] + c1r[nt][e], Y1[nt][e]);
+                                    Y2[nt][e] = fma(sc, c2[nt][e], Y2[nt][e]);
+                                    YG[nt][e] = fma(sc, c1o[nt][e] + cg[nt][e], YG[nt][e]);
+                                }
                         }
                         // emission (owner rows o0+lr, points qg+nt*8+2lc+e)
                         const int o = o0 + lr;
@@ -359,14 +436,13 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 const int q = qg + nt * 8 + 2 * lc + e;
-                                const double f = W(fcat, o, q) * dt;
-                                const double y1 = on[nt][e] ? f * acc[0][nt][e] : 0.0;
-                                const double y2 = on[nt][e] ? f * acc[1][nt][e] : 0.0;
-                                const double y3 = on[nt][e] ? f * acc[2][nt][e] : 0.0;
-                                dadd_cat<NT>(D, fcat, nt, e, -y1);
-                                dadd_cat<NT>(D, pd, nt, e, y2);
+                                const double f = on[nt][e] ? W(fcat, o, q) * dt : 0.0;
+                                const double y1 = f * Y1[nt][e];
+                                const double y2 = f * Y2[nt][e];
+                                const double y3 = f * (YG[nt][e] - Y2[nt][e]);
                                 const double up = __shfl_up_sync(0xffffffffu, y3, 4);
-                                if (lr > 0) dadd_cat<NT>(D, pd, nt, e, up);
+                                dadd_cat<NT>(D, fcat, nt, e, -y1);
+                                dadd_cat<NT>(D, pd, nt, e, lr > 0 ? y2 + up : y2);
                                 if (lr == 7) carry[(static_cast<size_t>(pd) * RB + b) * NP + q] += y3;
                             }
                     }
@@ -553,6 +629,11 @@ inline int launch_dmma(const DmmaTables &T, const FastTables &FT, const StepArgs
     DmmaArgs F{};
     F.S = S;
     F.RB = RB;
+    for (int X = 0; X < 2; ++X)
+        for (int b = 0; b < 8; ++b) {
+            F.kf[X][b] = T.kf[X][b];
+            F.km[X][b] = T.km[X][b];
+        }
     F.tail = tail;
     F.QP = QP;
     F.nbatches = (A.nactive_host + NP - 1) / NP;
