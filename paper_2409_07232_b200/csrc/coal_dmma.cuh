@@ -214,11 +214,15 @@ __global__ void __launch_bounds__(384, 1)
     int *pfail = reinterpret_cast<int *>(pidx + NP);                             // [NP]
     double *dstage = tabs; // [6][nkr][NP] at substep end (tables are idle then)
     __shared__ unsigned long long cta_act;
+    __shared__ int relcnt[2];
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int wid = tid >> 5, lane = tid & 31;
     const bool is_mma = wid < G * RB;
-    const int g = is_mma ? wid / RB : 0, b = is_mma ? wid % RB : 0;
+    // block b of group g: rotate by g so each SMSP (wid % 4) hosts a mix of blocks
+    // (the lower-triangular gain work grows with b)
+    const int g = is_mma ? wid / RB : 0, b = is_mma ? (wid % RB + g) % RB : 0;
+    const int NW = nthr >> 5;
     const int o0 = 8 * b;
     const int lr = lane >> 2, lc = lane & 3;
     const uint32_t nact = *A.nactive;
@@ -257,13 +261,12 @@ __global__ void __launch_bounds__(384, 1)
             ptrip[q] = 0;
         }
         __syncthreads();
-        for (int f = tid; f < kNCat * S * NP; f += nthr) { // q fastest: conflict-free STS
-            const int q = f % NP;
-            const int k = (f / NP) % S;
-            const int c = f / (NP * S);
-            const uint32_t p = pidx[q];
-            W(c, k, q) = (p != 0xffffffffu && k < nkr) ? A.bins[c][static_cast<size_t>(p) * nkr + k] : 0.0;
-        }
+        for (int c = 0; c < kNCat; ++c) // q across lanes: conflict-free STS
+            for (int k = wid; k < S; k += NW)
+                for (int q = lane; q < NP; q += 32) {
+                    const uint32_t p = pidx[q];
+                    W(c, k, q) = (p != 0xffffffffu && k < nkr) ? A.bins[c][static_cast<size_t>(p) * nkr + k] : 0.0;
+                }
         if (!gains_ready) {
             mbar_wait(&mbar[2], 0);
             gains_ready = true;
@@ -304,25 +307,35 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) D[c][nt][0] = D[c][nt][1] = 0.0;
 
-            // first pair's tables
+            // Pair pipeline without CTA barriers: tables of pairs n and n+1 are in flight
+            // in the two buffers; the LAST warp to release buffer (n&1) issues the TMA of
+            // pair n+2 into it, so warps drift and one warp's emission overlaps another
+            // warp's DMMAs.  full = mbar[buf] (TMA transaction), empty = relcnt[buf].
+            auto next_pair = [&](int p) -> int {
+                if (p < 0) return -1;
+                const unsigned long long rest = amask & ~((2ull << p) - 1ull);
+                return rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
+            };
+            const uint32_t tbytes = static_cast<uint32_t>(4 * TBL * sizeof(double));
             int cur = amask ? __ffsll(static_cast<long long>(amask)) - 1 : -1;
             int n = 0;
-            if (tid == 0 && cur >= 0) {
+            if (tid == 0) {
+                relcnt[0] = relcnt[1] = 0;
                 fence_proxy_async(); // dstage (generic writes) -> TMA overwrite
-                mbar_expect_tx(&mbar[0], static_cast<uint32_t>(4 * TBL * sizeof(double)));
-                tma_bulk_g2s(tabs, F.blob + static_cast<size_t>(cur) * 4 * TBL,
-                             static_cast<uint32_t>(4 * TBL * sizeof(double)), &mbar[0]);
+                if (cur >= 0) {
+                    mbar_expect_tx(&mbar[0], tbytes);
+                    tma_bulk_g2s(tabs, F.blob + static_cast<size_t>(cur) * 4 * TBL, tbytes, &mbar[0]);
+                }
+                const int p1 = next_pair(cur);
+                if (p1 >= 0) {
+                    mbar_expect_tx(&mbar[1], tbytes);
+                    tma_bulk_g2s(tabs + 4 * TBL, F.blob + static_cast<size_t>(p1) * 4 * TBL, tbytes, &mbar[1]);
+                }
             }
+            __syncthreads();
             while (cur >= 0) {
                 const int buf = n & 1;
-                const unsigned long long rest = amask & ~((2ull << cur) - 1ull);
-                const int nxt = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
-                if (tid == 0 && nxt >= 0) { // prefetch next pair into the other buffer
-                    fence_proxy_async();
-                    mbar_expect_tx(&mbar[buf ^ 1], static_cast<uint32_t>(4 * TBL * sizeof(double)));
-                    tma_bulk_g2s(tabs + (buf ^ 1) * 4 * TBL, F.blob + static_cast<size_t>(nxt) * 4 * TBL,
-                                 static_cast<uint32_t>(4 * TBL * sizeof(double)), &mbar[buf ^ 1]);
-                }
+                const int nxt = next_pair(cur);
                 mbar_wait(&mbar[buf], use[buf] & 1u);
                 use[buf] += 1;
                 const double *tb = tabs + buf * 4 * TBL;
@@ -523,10 +536,27 @@ __global__ void __launch_bounds__(384, 1)
                             }
                     }
                 }
-                __syncthreads(); // buffer `buf` free for the prefetch two pairs ahead
+                // release buffer `buf`; the last warp out refills it with pair n+2
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    const int old = atomicAdd(&relcnt[buf], 1);
+                    if (old == NW - 1) {
+                        relcnt[buf] = 0;
+                        __threadfence_block();
+                        const int p2 = next_pair(nxt);
+                        if (p2 >= 0) {
+                            fence_proxy_async();
+                            mbar_expect_tx(&mbar[buf], tbytes);
+                            tma_bulk_g2s(tabs + buf * 4 * TBL, F.blob + static_cast<size_t>(p2) * 4 * TBL,
+                                         tbytes, &mbar[buf]);
+                        }
+                    }
+                }
                 cur = nxt;
                 ++n;
             }
+            __syncthreads(); // every warp is done with the last tables before dstage reuses them
             // ---- combine deltas into dstage[c][o][q] (tables are idle now) ----
             if (is_mma) {
                 const int qg = g * NT * 8;
@@ -557,19 +587,18 @@ __global__ void __launch_bounds__(384, 1)
             }
             __syncthreads();
             // ---- Jacobi apply + stiffness (coalescence.cpp:313-328) ----
-            for (int f = tid; f < kNCat * nkr * NP; f += nthr) {
-                const int q = f % NP;
-                const int k = (f / NP) % nkr;
-                const int c = f / (NP * nkr);
-                const uint32_t p = pidx[q];
-                if (p == 0xffffffffu) continue;
-                const double v = W(c, k, q) + dstage[f];
-                W(c, k, q) = v;
-                if (v < 0.0 && pfail[q] == 0) {
-                    report_stiffness(A, p, c, k);
-                    pfail[q] = 2;
-                }
-            }
+            for (int c = 0; c < kNCat; ++c)
+                for (int k = wid; k < nkr; k += NW)
+                    for (int q = lane; q < NP; q += 32) {
+                        const uint32_t p = pidx[q];
+                        if (p == 0xffffffffu) continue;
+                        const double v = W(c, k, q) + dstage[(static_cast<size_t>(c) * nkr + k) * NP + q];
+                        W(c, k, q) = v;
+                        if (v < 0.0 && pfail[q] == 0) {
+                            report_stiffness(A, p, c, k);
+                            pfail[q] = 2;
+                        }
+                    }
             __syncthreads();
             for (int q = tid; q < NP; q += nthr)
                 if (pfail[q] == 2) pfail[q] = 3;
@@ -577,13 +606,12 @@ __global__ void __launch_bounds__(384, 1)
             __syncthreads();
         }
         // ---- write back + counters ----
-        for (int f = tid; f < kNCat * nkr * NP; f += nthr) {
-            const int q = f % NP;
-            const int k = (f / NP) % nkr;
-            const int c = f / (NP * nkr);
-            const uint32_t p = pidx[q];
-            if (p != 0xffffffffu) A.bins[c][static_cast<size_t>(p) * nkr + k] = W(c, k, q);
-        }
+        for (int c = 0; c < kNCat; ++c)
+            for (int k = wid; k < nkr; k += NW)
+                for (int q = lane; q < NP; q += 32) {
+                    const uint32_t p = pidx[q];
+                    if (p != 0xffffffffu) A.bins[c][static_cast<size_t>(p) * nkr + k] = W(c, k, q);
+                }
         for (int q = tid; q < NP; q += nthr) {
             if (pidx[q] == 0xffffffffu || pfail[q] != 0) continue;
             tr_acc += ptrip[q];
