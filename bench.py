@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank owns a full C2-shaped i-slab of an N x C2 domain "
+                         "(stacked in i); strong: the C2 domain is split across ranks")
     return ap.parse_args()
 
 
@@ -71,12 +74,6 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
-
-
-def slab(ni, world, rank):
-    base, rem = divmod(ni, world)  # near-equal split (decompose, driver.cpp:35-51)
-    i0 = rank * base + min(rank, rem)
-    return i0, i0 + base + (1 if rank < rem else 0)
 
 
 class ClockSampler:
@@ -219,11 +216,14 @@ def run_reference_arm(args):
 
 
 def config_block(args, world):
-    return {"workload": f"C2 CONUS-12km {args.ni}x{args.nj}x{args.nk} (i x j x k), "
+    scale = getattr(args, "scaling", "weak")
+    ni_g = args.ni * world if scale == "weak" else args.ni
+    return {"workload": f"C2 CONUS-12km {args.ni}x{args.nj}x{args.nk} (i x j x k) per GPU"
+                        f"{' (weak: N stacked C2 slabs)' if scale == 'weak' and world > 1 else ''}, "
                         f"{args.nkr} bins, thunderstorm all-category input, cf {args.cf}, "
                         f"dt 1 s, 1 substep",
             "grid": [args.ni, args.nj, args.nk], "nkr": args.nkr, "pairs": 20,
-            "global_points": args.ni * args.nj * args.nk,
+            "global_points": ni_g * args.nj * args.nk,
             "parallelism": f"i-slab shards x{world} (no halo; NCCL diagnostics only)",
             "numerics": args.numerics,
             "l2": "state (6 x 1.68 GB) >> 126 MB L2, and restored before every step"}
@@ -239,7 +239,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2409_07232_b200 as fsbm
-    from paper_2409_07232_b200 import _lib, synth
+    from paper_2409_07232_b200 import _lib, shard, synth
 
     world, rank, local = dist_env()
     if world > 1:
@@ -250,9 +250,10 @@ def run_ours(args):
 
     ctx, grid, tabs = make_ctx(args.nkr, local)
     nkr = args.nkr
-    T, P, _ = thermo(args, grid)
-    i0, i1 = slab(args.ni, world, rank)
-    state, mask = synth.thunderstorm_device(ctx, args.ni, args.nk, args.nj, args.cf,
+    ni_global = args.ni * world if args.scaling == "weak" else args.ni
+    T, P, _ = synth.thermo_host(ni_global, args.nk, args.nj, args.cf, CONFIG["seed"], grid)
+    i0, i1 = shard.slab(ni_global, world, rank)
+    state, mask = synth.thunderstorm_device(ctx, ni_global, args.nk, args.nj, args.cf,
                                             CONFIG["seed"], device=dev, i_slab=(i0, i1),
                                             thermo=(T, P, None))
     pristine = [b.clone() for b in state.bins]
@@ -302,21 +303,19 @@ def run_ours(args):
         wall = time.perf_counter() - wall0
     step_ms = sum(a.elapsed_time(b) for a, b in zip(e_beg, e_end)) / args.steps
     kernel_ms = sum(kern_ms) / len(kern_ms)
-    # diagnostics (NCCL all-reduce): points, triples, mass before/after one step
+    # diagnostics (the only collective: one NCCL all-reduce of a few scalars)
     restore()
     m0 = mass()
     fsbm.fissioned_step(state, mask, fsbm.StepContext(ctx, sctx.coal, None, stream=stream.cuda_stream), plan)
     m1 = mass()
-    diag = torch.tensor([float(cnt.points) / args.steps, float(cnt.triples) / args.steps,
-                         m0.item(), m1.item(), step_ms, kernel_ms],
-                        dtype=torch.float64, device=dev)
+    diag = shard.reduce_diagnostics(
+        shard.StepDiagnostics(cnt.triples // args.steps, cnt.points // args.steps,
+                              cnt.kernel_evals // args.steps, m0.item(), m1.item()), dist, dev)
+    tmax = torch.tensor([step_ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        summ = diag[:4].clone()
-        dist.all_reduce(summ, op=dist.ReduceOp.SUM)
-        mx = diag[4:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        diag = torch.cat([summ, mx])
-    points, triples, m0g, m1g, step_ms_max, kernel_ms_max = diag.tolist()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)  # device time: max over ranks
+    step_ms_max, kernel_ms_max = tmax.tolist()
+    points, triples, m0g, m1g = float(diag.points), float(diag.triples), diag.mass_before, diag.mass_after
     value = points / (step_ms_max * 1e-3)
 
     # ---- roofline (FP64 pipe; algorithmic flops) ----
@@ -366,7 +365,7 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (SURVEY 8(d) thunderstorm builder; golovin tables)",
                 "config": config_block(args, world),
                 "e2e": e2e, "gpu_launches": launches * world,
