@@ -45,7 +45,8 @@
 
 namespace fsbm {
 
-constexpr int kDmmaRB = 4; // full 8-row blocks handled by this kernel (nkr = 32 or 33)
+constexpr int kDmmaRB = 4;   // full 8-row blocks handled by this kernel (nkr = 32 or 33)
+constexpr int kDmmaNBUF = 3; // per-pair table buffers in flight (TMA lookahead)
 
 struct DmmaTables {
     int nkr = 0, S = 0, npairs = 0;
@@ -264,19 +265,20 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const int nkr = A.nkr, S = F.S, QP = F.QP, TAIL = F.tail;
     const int KS = S / 4;
     const size_t TBL = static_cast<size_t>(S) * S;
-    double *tabs = reinterpret_cast<double *>(smem_raw);                 // [2][T500|Kd][S][S]
-    double *gains = tabs + 4 * TBL;                                        // [lo|hi][S][S]
+    constexpr int NBUF = kDmmaNBUF;
+    double *tabs = reinterpret_cast<double *>(smem_raw);                 // [NBUF][T500|Kd][S][S]
+    double *gains = tabs + 2 * NBUF * TBL;                                 // [lo|hi][S][S]
     double *work = gains + 2 * TBL;                                        // [6][S][QP]
     double *carry = work + static_cast<size_t>(kNCat) * S * QP;            // [6][RB][NP]
     double *tdel = carry + static_cast<size_t>(kNCat) * RB * NP;           // [6][NP]
     double *wts = tdel + static_cast<size_t>(kNCat) * NP;                  // [NP]
     unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP);
     unsigned long long *ptrip = act + NP;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);             // [3]
-    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + 3);               // [NP]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);             // [NBUF tables, gains]
+    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + NBUF + 1);        // [NP]
     int *pfail = reinterpret_cast<int *>(pidx + NP);                       // [NP]
     __shared__ unsigned long long cta_act;
-    __shared__ int relcnt[2];
+    __shared__ int relcnt[kDmmaNBUF];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
     const int wid = tid >> 5, lane = tid & 31;
@@ -287,6 +289,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const int qg = g * NT * 8;
     const bool tail_warp = TAIL > 0 && b == 0; // block 0 is the lightest: it takes the top row
     const int ot = 8 * RB;                     // the tail (top) row, when TAIL == 1
+    if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const uint32_t nact = *A.nactive;
     const int npairs = A.pairs.npairs;
     const unsigned long long full_evals = static_cast<unsigned long long>(npairs) * nkr * nkr;
@@ -300,20 +303,19 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     };
 
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
-        mbar_init(&mbar[2], 1);
+        for (int i = 0; i <= NBUF; ++i) mbar_init(&mbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0) { // pair-independent gain coefficients, once per CTA
-        mbar_expect_tx(&mbar[2], static_cast<uint32_t>(2 * TBL * sizeof(double)));
-        tma_bulk_g2s(gains, F.gains, static_cast<uint32_t>(2 * TBL * sizeof(double)), &mbar[2]);
+        mbar_expect_tx(&mbar[NBUF], static_cast<uint32_t>(2 * TBL * sizeof(double)));
+        tma_bulk_g2s(gains, F.gains, static_cast<uint32_t>(2 * TBL * sizeof(double)), &mbar[NBUF]);
     }
-    uint32_t use[2] = {0u, 0u};
+    uint32_t pbase = 0; // pairs processed so far: pair #m uses buffer m % NBUF, phase (m / NBUF) & 1
     bool gains_ready = false;
 
-    for (uint32_t batch = blockIdx.x; batch < F.nbatches; batch += gridDim.x) {
+    for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
+         batch += gridDim.x) {
         for (int q = tid; q < NP; q += nthr) {
             const uint32_t idx = batch * static_cast<uint32_t>(NP) + q;
             const bool live = idx < nact;
@@ -324,14 +326,18 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             ptrip[q] = 0;
         }
         __syncthreads();
-        for (int c = 0; c < kNCat; ++c) // q across lanes: conflict-free STS
-            for (int k = wid; k < S; k += NW)
-                for (int q = lane; q < NP; q += 32) {
-                    const uint32_t p = pidx[q];
-                    W(c, k, q) = (p != 0xffffffffu && k < nkr) ? A.bins[c][static_cast<size_t>(p) * nkr + k] : 0.0;
-                }
+        for (int k = wid; k < S; k += NW) // q across lanes: conflict-free STS; 6 loads in flight
+            for (int q = lane; q < NP; q += 32) {
+                const uint32_t p = pidx[q];
+                const bool ok = p != 0xffffffffu && k < nkr;
+                double v[kNCat];
+#pragma unroll
+                for (int c = 0; c < kNCat; ++c) v[c] = ok ? __ldg(A.bins[c] + static_cast<size_t>(p) * nkr + k) : 0.0;
+#pragma unroll
+                for (int c = 0; c < kNCat; ++c) W(c, k, q) = v[c];
+            }
         if (!gains_ready) {
-            mbar_wait(&mbar[2], 0);
+            mbar_wait(&mbar[NBUF], 0);
             gains_ready = true;
         }
         __syncthreads();
@@ -378,25 +384,25 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             };
             int cur = amask ? __ffsll(static_cast<long long>(amask)) - 1 : -1;
             int n = 0;
-            if (tid == 0) {
-                relcnt[0] = relcnt[1] = 0;
+            if (tid == 0) { // prime all buffers with the first NBUF active pairs
                 fence_proxy_async();
-                if (cur >= 0) {
-                    mbar_expect_tx(&mbar[0], tbytes);
-                    tma_bulk_g2s(tabs, F.blob + static_cast<size_t>(cur) * 2 * TBL, tbytes, &mbar[0]);
-                }
-                const int p1 = next_pair(cur);
-                if (p1 >= 0) {
-                    mbar_expect_tx(&mbar[1], tbytes);
-                    tma_bulk_g2s(tabs + 2 * TBL, F.blob + static_cast<size_t>(p1) * 2 * TBL, tbytes, &mbar[1]);
+                int pp = cur;
+                for (int i = 0; i < NBUF; ++i, pp = next_pair(pp)) {
+                    const int bi = (pbase + i) % NBUF;
+                    relcnt[bi] = 0;
+                    if (pp >= 0) {
+                        mbar_expect_tx(&mbar[bi], tbytes);
+                        tma_bulk_g2s(tabs + bi * 2 * TBL, F.blob + static_cast<size_t>(pp) * 2 * TBL, tbytes,
+                                     &mbar[bi]);
+                    }
                 }
             }
             __syncthreads();
             while (cur >= 0) {
-                const int buf = n & 1;
+                const uint32_t m = pbase + n;
+                const int buf = m % NBUF;
                 const int nxt = next_pair(cur);
-                mbar_wait(&mbar[buf], use[buf] & 1u);
-                use[buf] += 1;
+                mbar_wait(&mbar[buf], (m / NBUF) & 1u);
                 const double *T5 = tabs + buf * 2 * TBL;
                 const double *Td = T5 + TBL;
                 const double *Glo = gains, *Ghi = gains + TBL;
@@ -596,7 +602,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     if (old == NW - 1) {
                         relcnt[buf] = 0;
                         __threadfence_block();
-                        const int p2 = next_pair(nxt);
+                        int p2 = nxt; // pair n + NBUF
+                        for (int i = 1; i < NBUF; ++i) p2 = next_pair(p2);
                         if (p2 >= 0) {
                             fence_proxy_async();
                             mbar_expect_tx(&mbar[buf], tbytes);
@@ -608,6 +615,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 cur = nxt;
                 ++n;
             }
+            pbase += n;
             // ---- Jacobi apply (coalescence.cpp:313-328): every read of `work` for this
             // substep is done, so owners add their register deltas in place, then the
             // cross-block carries and the top row, then the stiffness scan.
@@ -675,9 +683,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
 inline size_t dmma_smem_bytes(int nkr, int S, int QP) {
     constexpr int NP = kDmmaNP;
     const size_t TBL = static_cast<size_t>(S) * S;
-    const size_t d = 6 * TBL + static_cast<size_t>(kNCat) * S * QP + static_cast<size_t>(kNCat) * kDmmaRB * NP +
+    const size_t d = (2 * kDmmaNBUF + 2) * TBL + static_cast<size_t>(kNCat) * S * QP + static_cast<size_t>(kNCat) * kDmmaRB * NP +
                      static_cast<size_t>(kNCat) * NP + NP;
-    return d * 8 + NP * 8 * 2 + 3 * 8 + NP * 4 + NP * 4;
+    return d * 8 + NP * 8 * 2 + (kDmmaNBUF + 1) * 8 + NP * 4 + NP * 4;
 }
 
 /// Returns -1 when this geometry cannot run the DMMA path (caller falls back).

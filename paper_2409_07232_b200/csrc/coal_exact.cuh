@@ -35,6 +35,7 @@ __device__ inline void flush_counters(const StepArgs &A, unsigned long long tr,
 }
 
 __global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, double *arena) {
+    if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const int nkr = A.nkr;
     const uint32_t nact = *A.nactive;
     const int lane = threadIdx.x & 31;

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const int rsub = lane % R, grp = lane / R;
     const int V = kFastWarps * R; // row slots per round
+    if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const uint32_t nact = *A.nactive;
     const int npairs = A.pairs.npairs;
     const unsigned long long full_evals = static_cast<unsigned long long>(npairs) * nkr * nkr;
@@ -217,7 +218,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
 
     unsigned long long tr_acc = 0, pt_acc = 0, ev_acc = 0;
 
-    for (uint32_t batch = blockIdx.x; batch < F.nbatches; batch += gridDim.x) {
+    for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(F.npts) < nact;
+         batch += gridDim.x) {
         // ---- load the batch: point ids, weights, spectra --------------------
         for (int q = tid; q < F.npts; q += nthr) {
             const uint32_t idx = batch * static_cast<uint32_t>(F.npts) + q;

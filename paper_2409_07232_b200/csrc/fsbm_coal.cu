@@ -81,19 +81,22 @@ struct fsbm_ctx {
     FastTables fast{};
     DmmaTables dmma{};
     int fast_kernel = 0; // 0 auto, 1 direct (coal_fast), 2 dmma (FSBM_FAST_KERNEL)
-    // per-step workspace (grown on demand, never per-step allocated in steady state)
-    void *d_ws = nullptr;
-    size_t ws_bytes = 0;
+    // per-step workspace (grown on demand, never per-step allocated in steady state):
+    // one compaction workspace per pipeline slot (the host path runs 3 chunks in flight)
+    static constexpr int kSlots = 3;
+    void *d_ws[kSlots] = {};
+    size_t ws_bytes[kSlots] = {};
+    double *d_chunk[kSlots] = {};  // host path: device staging of one i-chunk
+    size_t chunk_bytes[kSlots] = {};
+    cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
+    cudaStream_t s_in = nullptr, s_out = nullptr;
     double *d_arena = nullptr;
     size_t arena_bytes = 0;
     unsigned long long *d_sink = nullptr;  // {err_key, triples, points, evals, count}
     unsigned long long *h_sink = nullptr;  // pinned mirror
     int4 *d_tiles = nullptr;
     int tiles_cap = 0;
-    // host-path staging
-    double *d_state = nullptr;
-    size_t state_bytes = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr; // compute stream of the host path
     int num_sms = 148;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // brackets the coalescence kernel
     int last_launches = 0;
@@ -152,25 +155,32 @@ void free_ctx(fsbm_ctx *c) {
     cudaFree(c->d_gtop);
     free_fast_tables(c->fast);
     free_dmma_tables(c->dmma);
-    cudaFree(c->d_ws);
+    for (int k = 0; k < fsbm_ctx::kSlots; ++k) {
+        cudaFree(c->d_ws[k]);
+        cudaFree(c->d_chunk[k]);
+        if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+        if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
+        if (c->ev_out[k]) cudaEventDestroy(c->ev_out[k]);
+    }
     cudaFree(c->d_arena);
     cudaFree(c->d_sink);
     cudaFree(c->d_tiles);
-    cudaFree(c->d_state);
     if (c->h_sink) cudaFreeHost(c->h_sink);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     delete c;
 }
 
-int ensure_ws(fsbm_ctx *c, size_t bytes) {
-    if (bytes <= c->ws_bytes) return FSBM_OK;
-    cudaFree(c->d_ws);
-    c->d_ws = nullptr;
-    c->ws_bytes = 0;
-    FSBM_CUDA_TRY(cudaMalloc(&c->d_ws, bytes));
-    c->ws_bytes = bytes;
+int ensure_ws(fsbm_ctx *c, int slot, size_t bytes) {
+    if (bytes <= c->ws_bytes[slot]) return FSBM_OK;
+    cudaFree(c->d_ws[slot]);
+    c->d_ws[slot] = nullptr;
+    c->ws_bytes[slot] = 0;
+    FSBM_CUDA_TRY(cudaMalloc(&c->d_ws[slot], bytes));
+    c->ws_bytes[slot] = bytes;
     return FSBM_OK;
 }
 
@@ -256,92 +266,98 @@ int grid_for(size_t n, int threads = 256) {
     return static_cast<int>(std::min<size_t>(std::max<size_t>(b, 1), 148 * 16));
 }
 
-// ---- core: one device step over compacted mask-true points -----------------
+// ---- core: device steps over compacted mask-true points ----------------------
+//
+// A step is (validate) -> one or more enqueue_chunk() calls (each an i-slab of the
+// domain: flags + stale check, CUB compaction, one coalescence kernel, all
+// stream-ordered, no host sync) -> finalize() (one sync, sink read-back).  The
+// sink is {err_key, triples, points, evals, stale}; serial-order error keys are
+// domain-global, so chunks reduce with a plain min.
 
-int step_device(fsbm_ctx *c, fsbm_ranges r, double *const bins[FSBM_NCAT], const double *P,
-                const double *T, const uint8_t *mask, double dt, int substeps,
-                const fsbm_plan *plan_in, const fsbm_tile *tiles, int ntiles, cudaStream_t s,
-                fsbm_counters *counters_out, fsbm_error *err_out) {
-    fsbm_plan plan_default{0, 2, 1, FSBM_ON_DEMAND, FSBM_AUTOMATIC, FSBM_NUMERICS_FAST};
-    const fsbm_plan *plan = plan_in ? plan_in : &plan_default;
+struct StepGeom {
+    fsbm_ranges r;
+    int ni, nk, nj;  // global extents
+    size_t np;       // global points
+};
+
+int validate_step(fsbm_ctx *c, fsbm_ranges r, const double *P, const double *T,
+                  const uint8_t *mask, const fsbm_plan *plan, const fsbm_tile *tiles, int ntiles,
+                  StepGeom &g) {
     if (int st = validate_plan(plan)) return st;
     if (r.ide < r.ids || r.kde < r.kds || r.jde < r.jds)
         return fail(FSBM_SHAPE, "fissioned_step: empty or inverted ranges");
-    const int ni = r.ide - r.ids + 1, nk = r.kde - r.kds + 1, nj = r.jde - r.jds + 1;
-    const size_t np = static_cast<size_t>(ni) * nk * nj;
-    if (np >= (1ull << 32)) return fail(FSBM_SHAPE, "fissioned_step: more than 2^32 points");
+    g.r = r;
+    g.ni = r.ide - r.ids + 1;
+    g.nk = r.kde - r.kds + 1;
+    g.nj = r.jde - r.jds + 1;
+    g.np = static_cast<size_t>(g.ni) * g.nk * g.nj;
+    if (g.np >= (1ull << 32)) return fail(FSBM_SHAPE, "fissioned_step: more than 2^32 points");
     if (!mask && !T) return fail(FSBM_DOMAIN, "fissioned_step: need a mask or temperatures");
     if (!P) return fail(FSBM_DOMAIN, "fissioned_step: pressure is required");
-    for (int q = 0; q < FSBM_NCAT; ++q)
-        if (!bins[q]) return fail(FSBM_DOMAIN, "fissioned_step: null category array");
-    if (ntiles < 0 || (ntiles > 0 && !tiles))
-        return fail(FSBM_DOMAIN, "fissioned_step: bad tile list");
-
-    // workspace: flags (np) | active (np u32) | cub temp
-    size_t cub_bytes = 0;
-    thrust::counting_iterator<uint32_t> cnt_it(0);
-    cub::DeviceSelect::Flagged(nullptr, cub_bytes, cnt_it, static_cast<uint8_t *>(nullptr),
-                               static_cast<uint32_t *>(nullptr),
-                               static_cast<uint32_t *>(nullptr), static_cast<int>(np), s);
-    const size_t off_active = (np + 255) / 256 * 256;
-    const size_t off_nact = off_active + (np * 4 + 255) / 256 * 256;
-    const size_t off_cub = off_nact + 256;
-    if (int st = ensure_ws(c, off_cub + cub_bytes)) return st;
-    uint8_t *flags = static_cast<uint8_t *>(c->d_ws);
-    uint32_t *active = reinterpret_cast<uint32_t *>(static_cast<char *>(c->d_ws) + off_active);
-    uint32_t *nact = reinterpret_cast<uint32_t *>(static_cast<char *>(c->d_ws) + off_nact);
-    void *cub_tmp = static_cast<char *>(c->d_ws) + off_cub;
-
+    if (ntiles < 0 || (ntiles > 0 && !tiles)) return fail(FSBM_DOMAIN, "fissioned_step: bad tile list");
     if (ntiles > c->tiles_cap) {
         cudaFree(c->d_tiles);
         c->d_tiles = nullptr;
         FSBM_CUDA_TRY(cudaMalloc(&c->d_tiles, sizeof(int4) * ntiles));
         c->tiles_cap = ntiles;
     }
-    if (ntiles > 0)
-        FSBM_CUDA_TRY(cudaMemcpyAsync(c->d_tiles, tiles, sizeof(int4) * ntiles,
-                                      cudaMemcpyHostToDevice, s));
+    if (ntiles > 0) // tiny, synchronous: tiles are host memory of unknown lifetime
+        FSBM_CUDA_TRY(cudaMemcpy(c->d_tiles, tiles, sizeof(int4) * ntiles, cudaMemcpyHostToDevice));
+    return FSBM_OK;
+}
 
-    // sink: [0] err_key, [1..3] counters, [4] stale count
-    const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
+int begin_step(fsbm_ctx *c, cudaStream_t s) {
+    static const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
     FSBM_CUDA_TRY(cudaMemcpyAsync(c->d_sink, init, sizeof(init), cudaMemcpyHostToDevice, s));
     c->timed = false;
-    c->last_launches = 1;
-    flags_kernel<<<grid_for(np), 256, 0, s>>>(np, ni, nk, nj, r.ids, r.jds, mask, T,
-                                              ntiles > 0 ? c->d_tiles : nullptr, ntiles, flags,
-                                              c->d_sink + 4);
+    c->last_launches = 0;
+    return FSBM_OK;
+}
+
+/// Enqueue the step of i-rows [i0, i1) (0-based, global) whose arrays start at the
+/// given pointers; no host synchronisation.
+int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
+                  double *const bins[FSBM_NCAT], const double *P, const double *T,
+                  const uint8_t *mask, double dt, int substeps, const fsbm_plan *plan,
+                  int ntiles, cudaStream_t s, bool first, bool last) {
+    const int ni = i1 - i0;
+    const size_t np = static_cast<size_t>(ni) * g.nk * g.nj;
+    size_t cub_bytes = 0;
+    thrust::counting_iterator<uint32_t> cnt_it(0);
+    cub::DeviceSelect::Flagged(nullptr, cub_bytes, cnt_it, static_cast<uint8_t *>(nullptr),
+                               static_cast<uint32_t *>(nullptr), static_cast<uint32_t *>(nullptr),
+                               static_cast<int>(np), s);
+    const size_t off_active = (np + 255) / 256 * 256;
+    const size_t off_nact = off_active + (np * 4 + 255) / 256 * 256;
+    const size_t off_cub = off_nact + 256;
+    if (int st = ensure_ws(c, slot, off_cub + cub_bytes)) return st;
+    char *ws = static_cast<char *>(c->d_ws[slot]);
+    uint8_t *flags = reinterpret_cast<uint8_t *>(ws);
+    uint32_t *active = reinterpret_cast<uint32_t *>(ws + off_active);
+    uint32_t *nact = reinterpret_cast<uint32_t *>(ws + off_nact);
+    int4 *tl = ntiles > 0 ? c->d_tiles : nullptr;
+    flags_kernel<<<grid_for(np), 256, 0, s>>>(np, ni, g.nk, g.nj, g.r.ids + i0, g.r.jds, mask, T,
+                                              tl, ntiles, flags, c->d_sink + 4);
     FSBM_CUDA_TRY(cudaGetLastError());
-    cub::DeviceSelect::Flagged(cub_tmp, cub_bytes, cnt_it, flags, active, nact,
+    cub::DeviceSelect::Flagged(ws + off_cub, cub_bytes, cnt_it, flags, active, nact,
                                static_cast<int>(np), s);
     FSBM_CUDA_TRY(cudaGetLastError());
-    // read the active count and stale flag (needed for coal_step's argument checks)
-    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink + 4, c->d_sink + 4, sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, s));
-    uint32_t h_nact = 0;
-    FSBM_CUDA_TRY(cudaMemcpyAsync(&h_nact, nact, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    FSBM_CUDA_TRY(cudaStreamSynchronize(s));
-    if (mask && T && c->h_sink[4] != 0)
-        return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
-                                 "temperatures (stale predicate)");
-    if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
-    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
-    if (h_nact == 0) return FSBM_OK;
-    // coal_step argument checks (coalescence.cpp:206-209), raised only when called
-    if (!(dt > 0.0)) return fail(FSBM_DOMAIN, "coal_step: dt must be > 0");
-    if (substeps < 1) return fail(FSBM_DOMAIN, "coal_step: substeps must be >= 1");
 
     StepArgs A{};
     A.nkr = c->nkr;
     A.ni = ni;
-    A.nk = nk;
-    A.nj = nj;
-    A.ids = r.ids;
-    A.kds = r.kds;
-    A.jds = r.jds;
+    A.nk = g.nk;
+    A.nj = g.nj;
+    A.ids = g.r.ids;
+    A.kds = g.r.kds;
+    A.jds = g.r.jds;
+    A.i_off = i0;
+    A.ni_glob = g.ni;
+    A.stale = c->d_sink + 4;
     A.dt_sub = dt / substeps;
     A.substeps = substeps;
     A.kernel_strategy = plan->kernel_strategy;
-    A.nactive_host = h_nact;
+    A.nactive_host = static_cast<uint32_t>(np); // upper bound; kernels loop on the device count
     A.active = active;
     A.nactive = nact;
     for (int q = 0; q < FSBM_NCAT; ++q) A.bins[q] = bins[q];
@@ -354,18 +370,17 @@ int step_device(fsbm_ctx *c, fsbm_ranges r, double *const bins[FSBM_NCAT], const
     A.g_top = c->d_gtop;
     A.err_key = c->d_sink;
     A.counters = c->d_sink + 1;
-    A.tiles = ntiles > 0 ? c->d_tiles : nullptr;
+    A.tiles = tl;
     A.ntiles = ntiles;
     A.pairs = c->pairs;
 
-    FSBM_CUDA_TRY(cudaEventRecord(c->ev0, s));
+    if (first) FSBM_CUDA_TRY(cudaEventRecord(c->ev0, s));
     if (plan->numerics == FSBM_NUMERICS_EXACT) {
-        const int max_blocks = c->num_sms * 8;
-        const int blocks = static_cast<int>(std::min<size_t>(
-            (h_nact + kExactThreads - 1) / kExactThreads, static_cast<size_t>(max_blocks)));
-        const size_t warps = static_cast<size_t>(blocks) * (kExactThreads / 32);
+        const size_t blocks = std::min<size_t>((np + kExactThreads - 1) / kExactThreads,
+                                               static_cast<size_t>(c->num_sms) * 8);
+        const size_t warps = blocks * (kExactThreads / 32);
         if (int st = ensure_arena(c, warps * 2 * kNCat * c->nkr * 32 * sizeof(double))) return st;
-        coal_exact_kernel<<<blocks, kExactThreads, 0, s>>>(A, c->d_arena);
+        coal_exact_kernel<<<static_cast<int>(blocks), kExactThreads, 0, s>>>(A, c->d_arena);
         FSBM_CUDA_TRY(cudaGetLastError());
     } else {
         int st = -1;
@@ -376,33 +391,86 @@ int step_device(fsbm_ctx *c, fsbm_ranges r, double *const bins[FSBM_NCAT], const
             if (int st2 = launch_fast(c->fast, A, c->num_sms, s)) return fail(st2, fast_last_error());
         }
     }
-    FSBM_CUDA_TRY(cudaEventRecord(c->ev1, s));
-    c->timed = true;
-    c->last_launches = 2;
-    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink, c->d_sink, 4 * sizeof(unsigned long long),
+    if (last) {
+        FSBM_CUDA_TRY(cudaEventRecord(c->ev1, s));
+        c->timed = true;
+    }
+    c->last_launches += 2;
+    return FSBM_OK;
+}
+
+/// One sync, then counters / stale / stiffness from the sink.
+int finalize_step(fsbm_ctx *c, const StepGeom &g, cudaStream_t s, fsbm_counters *counters_out,
+                  fsbm_error *err_out) {
+    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink, c->d_sink, 5 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
     FSBM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
+    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+    if (c->h_sink[4] != 0)
+        return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
+                                 "temperatures (stale predicate)");
     if (counters_out) *counters_out = fsbm_counters{c->h_sink[1], c->h_sink[2], c->h_sink[3]};
     const unsigned long long key = c->h_sink[0];
-    if (key != ~0ull) {
-        const unsigned long long cb = key & ((1ull << 20) - 1);
-        const unsigned long long ord = key >> 20;
-        const unsigned long long in_tile = ord % np;
-        const int cat = static_cast<int>(cb / c->nkr), bin = static_cast<int>(cb % c->nkr);
-        const int i = static_cast<int>(in_tile % ni);
-        const int k = static_cast<int>((in_tile / ni) % nk);
-        const int j = static_cast<int>(in_tile / (static_cast<unsigned long long>(ni) * nk));
-        static const char *names[FSBM_NCAT] = {"liquid", "ice1", "ice2", "ice3", "snow",
-                                               "graupel"};
-        if (err_out)
-            *err_out = fsbm_error{cat, bin, 1, i + r.ids, k + r.kds, j + r.jds};
-        return fail(FSBM_STIFFNESS,
-                    "coal_step: bin " + std::to_string(bin) + " of category " + names[cat] +
-                        " would become negative; reduce dt or increase substeps at grid point "
-                        "(i=" + std::to_string(i + r.ids) + ", k=" + std::to_string(k + r.kds) +
-                        ", j=" + std::to_string(j + r.jds) + ")");
-    }
+    if (key == ~0ull) return FSBM_OK;
+    const unsigned long long cb = key & ((1ull << 20) - 1);
+    const unsigned long long in_tile = (key >> 20) % g.np;
+    const int cat = static_cast<int>(cb / c->nkr), bin = static_cast<int>(cb % c->nkr);
+    const int i = static_cast<int>(in_tile % g.ni);
+    const int k = static_cast<int>((in_tile / g.ni) % g.nk);
+    const int j = static_cast<int>(in_tile / (static_cast<unsigned long long>(g.ni) * g.nk));
+    static const char *names[FSBM_NCAT] = {"liquid", "ice1", "ice2", "ice3", "snow", "graupel"};
+    if (err_out) *err_out = fsbm_error{cat, bin, 1, i + g.r.ids, k + g.r.kds, j + g.r.jds};
+    return fail(FSBM_STIFFNESS,
+                "coal_step: bin " + std::to_string(bin) + " of category " + names[cat] +
+                    " would become negative; reduce dt or increase substeps at grid point (i=" +
+                    std::to_string(i + g.r.ids) + ", k=" + std::to_string(k + g.r.kds) +
+                    ", j=" + std::to_string(j + g.r.jds) + ")");
+}
+
+/// coal_step's argument checks (coalescence.cpp:206-209) fire only when a point runs;
+/// with invalid dt/substeps the number of mask-true points decides (slow path, sync).
+int count_active_sync(fsbm_ctx *c, const StepGeom &g, const uint8_t *mask, const double *T,
+                      int ntiles, cudaStream_t s, uint32_t *out) {
+    if (int st = begin_step(c, s)) return st;
+    size_t cub_bytes = 0;
+    thrust::counting_iterator<uint32_t> cnt_it(0);
+    cub::DeviceSelect::Flagged(nullptr, cub_bytes, cnt_it, static_cast<uint8_t *>(nullptr),
+                               static_cast<uint32_t *>(nullptr), static_cast<uint32_t *>(nullptr),
+                               static_cast<int>(g.np), s);
+    const size_t off_active = (g.np + 255) / 256 * 256;
+    const size_t off_nact = off_active + (g.np * 4 + 255) / 256 * 256;
+    if (int st = ensure_ws(c, 0, off_nact + 256 + cub_bytes)) return st;
+    char *ws = static_cast<char *>(c->d_ws[0]);
+    flags_kernel<<<grid_for(g.np), 256, 0, s>>>(g.np, g.ni, g.nk, g.nj, g.r.ids, g.r.jds, mask, T,
+                                                ntiles > 0 ? c->d_tiles : nullptr, ntiles,
+                                                reinterpret_cast<uint8_t *>(ws), c->d_sink + 4);
+    cub::DeviceSelect::Flagged(ws + off_nact + 256, cub_bytes, cnt_it, reinterpret_cast<uint8_t *>(ws),
+                               reinterpret_cast<uint32_t *>(ws + off_active),
+                               reinterpret_cast<uint32_t *>(ws + off_nact), static_cast<int>(g.np), s);
+    FSBM_CUDA_TRY(cudaGetLastError());
+    FSBM_CUDA_TRY(cudaMemcpyAsync(out, ws + off_nact, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink + 4, c->d_sink + 4, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
+    FSBM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (c->h_sink[4] != 0)
+        return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
+                                 "temperatures (stale predicate)");
     return FSBM_OK;
+}
+
+int check_step_args(fsbm_ctx *c, const StepGeom &g, const uint8_t *mask, const double *T,
+                    int ntiles, double dt, int substeps, cudaStream_t s, bool *nothing) {
+    *nothing = false;
+    if (dt > 0.0 && substeps >= 1) return FSBM_OK;
+    uint32_t n = 0;
+    if (int st = count_active_sync(c, g, mask, T, ntiles, s, &n)) return st;
+    if (n == 0) { // the reference never calls coal_step: no error, nothing to do
+        *nothing = true;
+        return FSBM_OK;
+    }
+    if (!(dt > 0.0)) return fail(FSBM_DOMAIN, "coal_step: dt must be > 0");
+    return fail(FSBM_DOMAIN, "coal_step: substeps must be >= 1");
 }
 
 // ---- synthetic thunderstorm spectra --------------------------
@@ -528,7 +596,16 @@ int fsbm_ctx_create(int device, int nkr, const double *x, double ratio, int npai
         if (cudaMalloc(&c->d_sink, 8 * sizeof(unsigned long long)) != cudaSuccess ||
             cudaMallocHost(&c->h_sink, 8 * sizeof(unsigned long long)) != cudaSuccess ||
             cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
+            st = fail(FSBM_CUDA, "fsbm_ctx_create: allocation failed");
+    }
+    if (!st) {
+        for (int k = 0; k < fsbm_ctx::kSlots && !st; ++k)
+            if (cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_out[k], cudaEventDisableTiming) != cudaSuccess)
             st = fail(FSBM_CUDA, "fsbm_ctx_create: allocation failed");
     }
     if (!st) {
@@ -581,64 +658,127 @@ int fsbm_fission_predicates_device(fsbm_ctx *c, size_t npoints, const double *T,
 
 int fsbm_step_grid_device(fsbm_ctx *c, fsbm_ranges ranges, double *const bins_d[FSBM_NCAT],
                           const double *pressure_d, const double *temperature_d,
-                          const uint8_t *mask_d, double dt, int substeps, const fsbm_plan *plan,
+                          const uint8_t *mask_d, double dt, int substeps, const fsbm_plan *plan_in,
                           const fsbm_tile *tiles, int ntiles, void *stream,
                           fsbm_counters *counters_out, fsbm_error *err_out) {
     if (!c) return fail(FSBM_DOMAIN, "fissioned_step: context must supply tables and gains");
-    DeviceGuard g(c->device);
-    return step_device(c, ranges, bins_d, pressure_d, temperature_d, mask_d, dt, substeps, plan,
-                       tiles, ntiles, static_cast<cudaStream_t>(stream), counters_out, err_out);
+    DeviceGuard dg(c->device);
+    fsbm_plan plan_default{0, 2, 1, FSBM_ON_DEMAND, FSBM_AUTOMATIC, FSBM_NUMERICS_FAST};
+    const fsbm_plan *plan = plan_in ? plan_in : &plan_default;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StepGeom g{};
+    if (int st = validate_step(c, ranges, pressure_d, temperature_d, mask_d, plan, tiles, ntiles, g))
+        return st;
+    for (int q = 0; q < FSBM_NCAT; ++q)
+        if (!bins_d[q]) return fail(FSBM_DOMAIN, "fissioned_step: null category array");
+    bool nothing = false;
+    if (int st = check_step_args(c, g, mask_d, temperature_d, ntiles, dt, substeps, s, &nothing))
+        return st;
+    if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
+    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+    if (nothing) return FSBM_OK;
+    if (int st = begin_step(c, s)) return st;
+    if (int st = enqueue_chunk(c, 0, g, 0, g.ni, bins_d, pressure_d, temperature_d, mask_d, dt,
+                               substeps, plan, ntiles, s, true, true))
+        return st;
+    return finalize_step(c, g, s, counters_out, err_out);
 }
 
 int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NCAT],
                         const double *pressure_h, const double *temperature_h,
-                        const uint8_t *mask_h, double dt, int substeps, const fsbm_plan *plan,
+                        const uint8_t *mask_h, double dt, int substeps, const fsbm_plan *plan_in,
                         const fsbm_tile *tiles, int ntiles, fsbm_counters *counters_out,
                         fsbm_error *err_out) {
     if (!c) return fail(FSBM_DOMAIN, "fissioned_step: context must supply tables and gains");
-    if (!pressure_h || (!temperature_h && !mask_h))
-        return fail(FSBM_DOMAIN, "fissioned_step: missing pressure/temperature/mask");
-    if (r.ide < r.ids || r.kde < r.kds || r.jde < r.jds)
-        return fail(FSBM_SHAPE, "fissioned_step: empty or inverted ranges");
-    DeviceGuard g(c->device);
-    const size_t np = static_cast<size_t>(r.ide - r.ids + 1) * (r.kde - r.kds + 1) *
-                      (r.jde - r.jds + 1);
-    const size_t bin_bytes = np * c->nkr * sizeof(double);
-    const size_t need = FSBM_NCAT * bin_bytes + 2 * np * sizeof(double) + np;
-    if (need > c->state_bytes) {
-        cudaFree(c->d_state);
-        c->d_state = nullptr;
-        c->state_bytes = 0;
-        cudaError_t e = cudaMalloc(&c->d_state, need);
-        if (e != cudaSuccess)
-            return fail(FSBM_ALLOC, "fissioned_step(host): cannot allocate " +
-                                        std::to_string(need) + " device bytes");
-        c->state_bytes = need;
+    DeviceGuard dg(c->device);
+    fsbm_plan plan_default{0, 2, 1, FSBM_ON_DEMAND, FSBM_AUTOMATIC, FSBM_NUMERICS_FAST};
+    const fsbm_plan *plan = plan_in ? plan_in : &plan_default;
+    StepGeom g{};
+    if (int st = validate_step(c, r, pressure_h, temperature_h, mask_h, plan, tiles, ntiles, g))
+        return st;
+    for (int q = 0; q < FSBM_NCAT; ++q)
+        if (!bins_h[q]) return fail(FSBM_DOMAIN, "fissioned_step: null category array");
+    const int nkr = c->nkr;
+    const size_t per_i = static_cast<size_t>(g.nk) * g.nj;
+    // Host-side stale check first: the reference raises before touching any point.
+    if (mask_h && temperature_h)
+        for (size_t p = 0; p < g.np; ++p) {
+            const double t = temperature_h[p];
+            if ((t > kOuterGateK && t > kCoalGateK) != (mask_h[p] != 0))
+                return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
+                                         "temperatures (stale predicate)");
+        }
+    if (!(dt > 0.0) || substeps < 1) {
+        size_t n = 0;
+        for (size_t p = 0; p < g.np; ++p) {
+            const bool on = mask_h ? mask_h[p] != 0
+                                   : (temperature_h[p] > kOuterGateK && temperature_h[p] > kCoalGateK);
+            n += on;
+        }
+        if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
+        if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+        if (n == 0) return FSBM_OK;
+        return fail(FSBM_DOMAIN, !(dt > 0.0) ? "coal_step: dt must be > 0" : "coal_step: substeps must be >= 1");
     }
-    char *base = reinterpret_cast<char *>(c->d_state);
-    double *bins_d[FSBM_NCAT];
-    for (int q = 0; q < FSBM_NCAT; ++q)
-        bins_d[q] = reinterpret_cast<double *>(base + q * bin_bytes);
-    double *P = reinterpret_cast<double *>(base + FSBM_NCAT * bin_bytes);
-    double *T = P + np;
-    uint8_t *M = reinterpret_cast<uint8_t *>(T + np);
-    cudaStream_t s = c->stream;
-    for (int q = 0; q < FSBM_NCAT; ++q)
-        FSBM_CUDA_TRY(cudaMemcpyAsync(bins_d[q], bins_h[q], bin_bytes, cudaMemcpyHostToDevice, s));
-    FSBM_CUDA_TRY(cudaMemcpyAsync(P, pressure_h, np * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (temperature_h)
-        FSBM_CUDA_TRY(cudaMemcpyAsync(T, temperature_h, np * sizeof(double),
-                                      cudaMemcpyHostToDevice, s));
-    if (mask_h) FSBM_CUDA_TRY(cudaMemcpyAsync(M, mask_h, np, cudaMemcpyHostToDevice, s));
-    int st = step_device(c, r, bins_d, P, temperature_h ? T : nullptr, mask_h ? M : nullptr, dt,
-                         substeps, plan, tiles, ntiles, s, counters_out, err_out);
-    if (st != FSBM_OK && st != FSBM_STIFFNESS) return st;
-    const std::string keep = g_err;
-    for (int q = 0; q < FSBM_NCAT; ++q)
-        FSBM_CUDA_TRY(cudaMemcpyAsync(bins_h[q], bins_d[q], bin_bytes, cudaMemcpyDeviceToHost, s));
-    FSBM_CUDA_TRY(cudaStreamSynchronize(s));
-    g_err = keep;
-    return st;
+    // Pipeline over i-chunks: H2D (s_in) -> flags/compaction/kernel (stream) -> D2H
+    // (s_out), kSlots chunks in flight; pinned host memory makes the copies async.
+    const int nchunks = std::max(1, std::min(g.ni, 8));
+    const int rows = (g.ni + nchunks - 1) / nchunks;
+    const size_t chunk_np = static_cast<size_t>(rows) * per_i;
+    const size_t need = FSBM_NCAT * chunk_np * nkr * sizeof(double) + 2 * chunk_np * sizeof(double) +
+                        chunk_np + 256;
+    for (int k = 0; k < fsbm_ctx::kSlots; ++k)
+        if (need > c->chunk_bytes[k]) {
+            cudaFree(c->d_chunk[k]);
+            c->d_chunk[k] = nullptr;
+            c->chunk_bytes[k] = 0;
+            if (cudaMalloc(&c->d_chunk[k], need) != cudaSuccess)
+                return fail(FSBM_ALLOC, "fissioned_step(host): cannot allocate " + std::to_string(need) +
+                                            " device bytes per pipeline slot");
+            c->chunk_bytes[k] = need;
+        }
+    cudaStream_t sc = c->stream;
+    if (int st = begin_step(c, sc)) return st;
+    FSBM_CUDA_TRY(cudaEventRecord(c->ev_comp[0], sc)); // sink init precedes every chunk
+    FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_in, c->ev_comp[0]));
+    int k = 0;
+    for (int i0 = 0; i0 < g.ni; i0 += rows, ++k) {
+        const int i1 = std::min(g.ni, i0 + rows);
+        const int slot = k % fsbm_ctx::kSlots;
+        const size_t p0 = static_cast<size_t>(i0) * per_i, np = static_cast<size_t>(i1 - i0) * per_i;
+        char *base = reinterpret_cast<char *>(c->d_chunk[slot]);
+        double *bd[FSBM_NCAT];
+        for (int q = 0; q < FSBM_NCAT; ++q)
+            bd[q] = reinterpret_cast<double *>(base + q * chunk_np * nkr * sizeof(double));
+        double *Pd = reinterpret_cast<double *>(base + FSBM_NCAT * chunk_np * nkr * sizeof(double));
+        double *Td = Pd + chunk_np;
+        uint8_t *Md = reinterpret_cast<uint8_t *>(Td + chunk_np);
+        if (k >= fsbm_ctx::kSlots) FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_in, c->ev_out[slot]));
+        for (int q = 0; q < FSBM_NCAT; ++q)
+            FSBM_CUDA_TRY(cudaMemcpyAsync(bd[q], bins_h[q] + p0 * nkr, np * nkr * sizeof(double),
+                                          cudaMemcpyHostToDevice, c->s_in));
+        FSBM_CUDA_TRY(cudaMemcpyAsync(Pd, pressure_h + p0, np * sizeof(double), cudaMemcpyHostToDevice, c->s_in));
+        if (temperature_h)
+            FSBM_CUDA_TRY(cudaMemcpyAsync(Td, temperature_h + p0, np * sizeof(double),
+                                          cudaMemcpyHostToDevice, c->s_in));
+        if (mask_h) FSBM_CUDA_TRY(cudaMemcpyAsync(Md, mask_h + p0, np, cudaMemcpyHostToDevice, c->s_in));
+        FSBM_CUDA_TRY(cudaEventRecord(c->ev_in[slot], c->s_in));
+        FSBM_CUDA_TRY(cudaStreamWaitEvent(sc, c->ev_in[slot]));
+        if (int st = enqueue_chunk(c, slot, g, i0, i1, bd, Pd, temperature_h ? Td : nullptr,
+                                   mask_h ? Md : nullptr, dt, substeps, plan, ntiles, sc, k == 0,
+                                   i1 == g.ni)) {
+            cudaStreamSynchronize(sc);
+            return st;
+        }
+        FSBM_CUDA_TRY(cudaEventRecord(c->ev_comp[slot], sc));
+        FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_out, c->ev_comp[slot]));
+        for (int q = 0; q < FSBM_NCAT; ++q)
+            FSBM_CUDA_TRY(cudaMemcpyAsync(bins_h[q] + p0 * nkr, bd[q], np * nkr * sizeof(double),
+                                          cudaMemcpyDeviceToHost, c->s_out));
+        FSBM_CUDA_TRY(cudaEventRecord(c->ev_out[slot], c->s_out));
+    }
+    FSBM_CUDA_TRY(cudaStreamSynchronize(c->s_out));
+    return finalize_step(c, g, sc, counters_out, err_out);
 }
 
 int fsbm_coal_step(fsbm_ctx *c, double *bins6, double pressure, double dt, int substeps,

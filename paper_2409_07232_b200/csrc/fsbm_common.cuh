@@ -32,8 +32,11 @@ struct PairTable {
 /// Everything a step kernel needs besides the state.
 struct StepArgs {
     int nkr;
-    int ni, nk, nj;            // domain extents
+    int ni, nk, nj;            // extents of this launch's slab (points p are slab-local)
     int ids, kds, jds;         // domain origin (1-based)
+    int i_off;                 // global i offset of the slab (host path processes i-chunks)
+    int ni_glob;               // global ni (serial-order keys are domain-global)
+    const unsigned long long *stale; // non-zero: stale mask detected -> do nothing
     double dt_sub;
     int substeps;
     int kernel_strategy;       // 0 precomputed / 1 on_demand (counters only)
@@ -58,7 +61,7 @@ struct StepArgs {
 __device__ inline unsigned long long order_key(const StepArgs &A, uint32_t p) {
     const uint32_t j = p % A.nj;
     const uint32_t k = (p / A.nj) % A.nk;
-    const uint32_t i = p / (A.nj * A.nk);
+    const uint32_t i = p / (A.nj * A.nk) + A.i_off; // global (0-based) i
     unsigned long long t = 0;
     if (A.tiles) {
         for (int q = 0; q < A.ntiles; ++q) {
@@ -67,8 +70,8 @@ __device__ inline unsigned long long order_key(const StepArgs &A, uint32_t p) {
             if (gi >= T.x && gi <= T.y && gj >= T.z && gj <= T.w) { t = q; break; }
         }
     }
-    const unsigned long long np = (unsigned long long)A.ni * A.nk * A.nj;
-    return t * np + ((unsigned long long)j * A.nk + k) * A.ni + i;
+    const unsigned long long np = (unsigned long long)A.ni_glob * A.nk * A.nj;
+    return t * np + ((unsigned long long)j * A.nk + k) * A.ni_glob + i;
 }
 
 __device__ inline void report_stiffness(const StepArgs &A, uint32_t p, int c, int bin) {
