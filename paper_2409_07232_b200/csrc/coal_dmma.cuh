@@ -411,7 +411,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
 
                 bool on[NT][2];
                 double we[NT][2];
-                bool all0 = true, all1 = true;
+                const double wu = wts[qg]; // first point of the warp's group
+                bool all0 = true, allu = true;
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -420,13 +421,15 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         on[nt][e] = act[q] >> cur & 1ull;
                         we[nt][e] = wts[q];
                         all0 = all0 && we[nt][e] == 0.0;
-                        all1 = all1 && we[nt][e] == 1.0;
+                        allu = allu && we[nt][e] == wu;
                     }
-                // Pressure-weight mode of the warp's 16 points (warp-uniform):
+                // Pressure-weight mode of the warp's 16 points (warp-uniform).  Points are
+                // compacted in GridState order (j fastest), so a group of 16 almost always
+                // sits on one model level and shares one pressure:
                 //   0: all w == 0 (p <= 500 hPa): K500 + Kd*0 == K500 exactly -> one half
-                //   1: all w == 1 (p >= 750 hPa): K = K500 + Kd, the reference's own sum
-                //   2: otherwise: K500 half + w * (Kd half)
-                const int wmode = __all_sync(0xffffffffu, all0) ? 0 : __all_sync(0xffffffffu, all1) ? 1 : 2;
+                //   1: all w == wu: K = K500 + wu*Kd interpolated in the A fragment -> one half
+                //   2: otherwise (group straddles a level): K500 half + w * (Kd half)
+                const int wmode = __all_sync(0xffffffffu, all0) ? 0 : __all_sync(0xffffffffu, allu) ? 1 : 2;
                 const double *vbase[2] = {&W(pb, lc, qg + lr), &W(pa, lc, qg + lr)};
 
                 for (int X = 0; X < (self ? 1 : 2); ++X) {
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         int ai = abase;
 #pragma unroll 2
                         for (int ks = 0; ks < kf; ++ks, ai += astride) { // every cell owned-far
-                            const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+                            const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
                             const double t2 = t * Glo[ai];
 #pragma unroll
                             for (int nt = 0; nt < NT; ++nt) {
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         }
                         for (int ks = kf; ks < km; ++ks, ai += astride) { // diagonal steps
                             const int s = 4 * ks + lc;
-                            const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+                            const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
                             // gain view: R-cross s<o, R-self s<o (+ s==o at 1/2), C s<=o
                             const double msk = V == 2 ? (s <= o ? 1.0 : 0.0)
                                                       : (s < o ? 1.0 : (V == 1 && s == o ? 0.5 : 0.0));
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         }
 #pragma unroll 2
                         for (int ks = km; ks < KS; ++ks, ai += astride) { // no owned gains
-                            const double t = summed ? T5[ai] + Td[ai] : Ta[ai];
+                            const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
 #pragma unroll
                             for (int nt = 0; nt < NT; ++nt) {
                                 const double v = vb[(4 * ks) * QP + nt * 8];
