@@ -12,6 +12,8 @@ import re
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_PKG, "_lib", "libfsbm_coal.so")
+# FSBM_LIB_PATH: load another build of the same C ABI (A/B kernel experiments)
+SO_PATH = os.environ.get("FSBM_LIB_PATH", SO_PATH)
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "fsbm_coal.h")
 
 NCAT = 6

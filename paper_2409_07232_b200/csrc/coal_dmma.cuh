@@ -36,6 +36,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -231,8 +233,31 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+#ifdef FSBM_DMMA_PROF // per-warp phase cycle counters (A/B profiling builds only)
+#define PROF_DECL                                                                                  \
+    unsigned long long pf[8] = {};                                                                 \
+    unsigned long long pt0 = clock64();
+#define PROF_MARK(k)                                                                               \
+    {                                                                                              \
+        const unsigned long long t1_ = clock64();                                                  \
+        pf[k] += t1_ - pt0;                                                                        \
+        pt0 = t1_;                                                                                 \
+    }
+#define PROF_FLUSH                                                                                 \
+    if (lane == 0 && F.prof)                                                                       \
+        for (int k = 0; k < 8; ++k) atomicAdd(F.prof + wid * 8 + k, pf[k]);
+#else
+#define PROF_DECL
+#define PROF_MARK(k)
+#define PROF_FLUSH
+#endif
+// phases: 0 batch setup, 1 tail, 2 table wait, 3 K-loops, 4 apply barrier, 5 apply..writeback,
+// 6 emission, 7 per-pair bookkeeping
+
 struct DmmaArgs {
+    unsigned long long *prof; // FSBM_DMMA_PROF builds: [warp][8] cycles per phase
     int S, tail, QP;
+    int std_classes; // kf == 2b, km == 2b + 2 in every view and S == 36: unrolled K-loops
     uint32_t nbatches;
     int kf[3][kDmmaRB], km[3][kDmmaRB];
     const double *blob, *gains;
@@ -257,6 +282,96 @@ __device__ __forceinline__ void dadd_cat(double (&D)[kNCat][kDmmaNT][2], int cat
     case 4: D[4][nt][e] += v; break;
     default: D[5][nt][e] += v; break;
     }
+}
+
+/// One single-half pass of a warp's 8-row block with compile-time K-step classes
+/// (full: ks < KF, diagonal: KF <= ks < KM, no owned gains: ks >= KM; KSN steps),
+/// fully unrolled so the A-fragment loads/interpolation are scheduled ahead of the
+/// DMMA chains.  INTERP: A = K500 + wu*Kd, else A = K500.
+template <int KF, int KM, int KSN, bool INTERP>
+__device__ __forceinline__ void dmma_pass_single(const double *__restrict__ T5, const double *__restrict__ Td,
+                                                 double wu, const double *__restrict__ Glo,
+                                                 const double *__restrict__ Ghi, int abase, int astride,
+                                                 const double *__restrict__ vb, int QP, int V, int o, int lc,
+                                                 double (&c1)[kDmmaNT][2], double (&c2)[kDmmaNT][2],
+                                                 double (&cg)[kDmmaNT][2]) {
+    double cf[kDmmaNT][2];
+#pragma unroll
+    for (int nt = 0; nt < kDmmaNT; ++nt) cf[nt][0] = cf[nt][1] = c2[nt][0] = c2[nt][1] = cg[nt][0] = cg[nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KSN; ++ks) {
+        const int ai = abase + ks * astride;
+        const double t = INTERP ? fma(wu, Td[ai], T5[ai]) : T5[ai];
+        if (ks < KF) { // every cell owned-far: Y3 = YG - Y2 shares the loss DMMAs
+            const double t2 = t * Glo[ai];
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                const double v = vb[(4 * ks) * QP + nt * 8];
+                dmma(cf[nt][0], cf[nt][1], t, v);
+                dmma(c2[nt][0], c2[nt][1], t2, v);
+            }
+        } else if (ks < KM) { // diagonal steps
+            const int s = 4 * ks + lc;
+            const double msk = V == 2 ? (s <= o ? 1.0 : 0.0) : (s < o ? 1.0 : (V == 1 && s == o ? 0.5 : 0.0));
+            const double lo = msk * Glo[ai], hi = msk * Ghi[ai];
+            const double t2 = t * lo, tg = t * (lo + hi);
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                const double v = vb[(4 * ks) * QP + nt * 8];
+                dmma(c1[nt][0], c1[nt][1], t, v);
+                dmma(c2[nt][0], c2[nt][1], t2, v);
+                dmma(cg[nt][0], cg[nt][1], tg, v);
+            }
+        } else { // no owned gains
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                const double v = vb[(4 * ks) * QP + nt * 8];
+                dmma(c1[nt][0], c1[nt][1], t, v);
+            }
+        }
+    }
+#pragma unroll
+    for (int nt = 0; nt < kDmmaNT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            c1[nt][e] += cf[nt][e];
+            cg[nt][e] += cf[nt][e];
+        }
+}
+
+typedef double DmmaAcc[kDmmaNT][2];
+
+/// D[FC] -= L, D[PD] += G with compile-time categories: one indirect branch per pass
+/// instead of a branch tree per value.
+template <int FC, int PD>
+__device__ __forceinline__ void emit_fp(double (&D)[kNCat][kDmmaNT][2], const DmmaAcc &L, const DmmaAcc &G) {
+#pragma unroll
+    for (int nt = 0; nt < kDmmaNT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            D[FC][nt][e] -= L[nt][e];
+            D[PD][nt][e] += G[nt][e];
+        }
+}
+
+__device__ __forceinline__ void emit_switch(int sel, double (&D)[kNCat][kDmmaNT][2], const DmmaAcc &L,
+                                            const DmmaAcc &G) {
+#define FSBM_EMIT_CASE(F, P)                                                                       \
+    case F * kNCat + P: emit_fp<F, P>(D, L, G); break;
+#define FSBM_EMIT_ROW(F)                                                                           \
+    FSBM_EMIT_CASE(F, 0) FSBM_EMIT_CASE(F, 1) FSBM_EMIT_CASE(F, 2) FSBM_EMIT_CASE(F, 3)            \
+    FSBM_EMIT_CASE(F, 4) FSBM_EMIT_CASE(F, 5)
+    switch (sel) {
+        FSBM_EMIT_ROW(0)
+        FSBM_EMIT_ROW(1)
+        FSBM_EMIT_ROW(2)
+        FSBM_EMIT_ROW(3)
+        FSBM_EMIT_ROW(4)
+        FSBM_EMIT_ROW(5)
+    default: break;
+    }
+#undef FSBM_EMIT_ROW
+#undef FSBM_EMIT_CASE
 }
 
 __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, DmmaArgs F) {
@@ -287,7 +402,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const int o0 = 8 * b;
     const int lr = lane >> 2, lc = lane & 3;
     const int qg = g * NT * 8;
-    const bool tail_warp = TAIL > 0 && b == 0; // block 0 is the lightest: it takes the top row
     const int ot = 8 * RB;                     // the tail (top) row, when TAIL == 1
     if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const uint32_t nact = *A.nactive;
@@ -313,6 +427,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     }
     uint32_t pbase = 0; // pairs processed so far: pair #m uses buffer m % NBUF, phase (m / NBUF) & 1
     bool gains_ready = false;
+    PROF_DECL
 
     for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
          batch += gridDim.x) {
@@ -370,6 +485,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             __syncthreads();
             const unsigned long long amask = cta_act;
 
+            PROF_MARK(0)
             double D[kNCat][NT][2];
 #pragma unroll
             for (int c = 0; c < kNCat; ++c)
@@ -402,7 +518,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 const uint32_t m = pbase + n;
                 const int buf = m % NBUF;
                 const int nxt = next_pair(cur);
+                PROF_MARK(7)
                 mbar_wait(&mbar[buf], (m / NBUF) & 1u);
+                PROF_MARK(2)
                 const double *T5 = tabs + buf * 2 * TBL;
                 const double *Td = T5 + TBL;
                 const double *Glo = gains, *Ghi = gains + TBL;
@@ -446,7 +564,37 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     for (int nt = 0; nt < NT; ++nt)
                         Y1[nt][0] = Y1[nt][1] = Y2[nt][0] = Y2[nt][1] = YG[nt][0] = YG[nt][1] = 0.0;
                     const int nhalf = wmode == 2 ? 2 : 1;
-                    for (int h = 0; h < nhalf; ++h) {
+                    const bool unrolled = F.std_classes && wmode != 2;
+                    if (unrolled) { // fully unrolled K-loops (the common case)
+                        double c1[NT][2] = {}, c2[NT][2], cg[NT][2];
+#define FSBM_PASS(BB, IN)                                                                          \
+    dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN>(T5, Td, wu, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg)
+                        if (wmode == 1) {
+                            switch (b) {
+                            case 0: FSBM_PASS(0, true); break;
+                            case 1: FSBM_PASS(1, true); break;
+                            case 2: FSBM_PASS(2, true); break;
+                            default: FSBM_PASS(3, true); break;
+                            }
+                        } else {
+                            switch (b) {
+                            case 0: FSBM_PASS(0, false); break;
+                            case 1: FSBM_PASS(1, false); break;
+                            case 2: FSBM_PASS(2, false); break;
+                            default: FSBM_PASS(3, false); break;
+                            }
+                        }
+#undef FSBM_PASS
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                Y1[nt][e] = c1[nt][e];
+                                Y2[nt][e] = c2[nt][e];
+                                YG[nt][e] = cg[nt][e];
+                            }
+                    }
+                    for (int h = 0; h < (unrolled ? 0 : nhalf); ++h) {
                         const double *Ta = h == 0 ? T5 : Td;
                         const bool summed = wmode == 1;
                         double c1[NT][2], c2[NT][2], cg[NT][2];
@@ -506,61 +654,53 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                                 YG[nt][e] = fma(sc, cg[nt][e], YG[nt][e]);
                             }
                     }
+                    PROF_MARK(3)
                     // emission: rows o, points qg+nt*8+2lc+e; hi-gain -> row o+1
+                    DmmaAcc L, Gn;
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int q = qg + nt * 8 + 2 * lc + e;
-                            const double f = on[nt][e] ? W(fcat, o, q) * dt : 0.0;
+                            const double f = on[nt][e] ? W(fcat, o, q) : 0.0; // dt: applied at the apply
                             const double y3 = f * (YG[nt][e] - Y2[nt][e]);
                             const double up = __shfl_up_sync(0xffffffffu, y3, 4);
-                            dadd_cat(D, fcat, nt, e, -f * Y1[nt][e]);
-                            dadd_cat(D, pd, nt, e, lr > 0 ? fma(f, Y2[nt][e], up) : f * Y2[nt][e]);
+                            L[nt][e] = f * Y1[nt][e];
+                            Gn[nt][e] = lr > 0 ? fma(f, Y2[nt][e], up) : f * Y2[nt][e];
                             if (lr == 7) carry[(static_cast<size_t>(pd) * RB + b) * NP + q] += y3;
                         }
+                    emit_switch(fcat * kNCat + pd, D, L, Gn);
 
-                    // the top row as a 4-row DMMA tile: rows {P1^500, P2^500, P1^d, P2^d}
-                    if (tail_warp) {
-                        double c[NT][2];
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
-                        const bool use_d = (lr & 2) != 0, use_g = (lr & 1) != 0;
-                        const double *Tt = use_d ? Td : T5;
-                        for (int ks = 0; ks < KS; ++ks) {
-                            const int s = 4 * ks + lc;
-                            const int ti = X == 0 ? ot * S + s : s * S + ot;
-                            double a = lr < 4 ? Tt[ti] : 0.0;
-                            if (use_g) {
-                                const double msk = V == 2 ? (s <= ot ? 1.0 : 0.0)
-                                                          : (s < ot ? 1.0 : (V == 1 && s == ot ? 0.5 : 0.0));
-                                a *= msk * Glo[V == 1 && s == ot ? ot * S + ot : ti];
-                            }
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) {
-                                const double v = vb[(4 * ks) * QP + nt * 8];
-                                dmma(c[nt][0], c[nt][1], a, v);
-                            }
+                    PROF_MARK(6)
+                    // the top row (bin nkr-1, nkr % 8 == 1): a 1-row GEMM is 1/8 of a DMMA tile, so
+                    // it runs on the FP64 CUDA cores, balanced over the group's four warps:
+                    // warp b takes points 4b..4b+3 of the group, 8 lanes per point split s.
+                    if (TAIL > 0) {
+                        const int qt = qg + 4 * b + (lane >> 3), sc0 = lane & 7;
+                        const double wq = wts[qt];
+                        const double *vt = &W(X == 0 ? pb : pa, 0, qt);
+                        double y1 = 0.0, y2 = 0.0;
+                        for (int sx = sc0; sx < nkr; sx += 8) {
+                            const int ti = X == 0 ? ot * S + sx : sx * S + ot;
+                            const double m = V == 2 ? (sx <= ot ? 1.0 : 0.0)
+                                                    : (sx < ot ? 1.0 : (V == 1 && sx == ot ? 0.5 : 0.0));
+                            const double kv = fma(wq, Td[ti], T5[ti]) * vt[static_cast<size_t>(sx) * QP];
+                            y1 += kv;
+                            y2 = fma(kv, m * Glo[ti], y2);
                         }
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const double p2 = __shfl_down_sync(0xffffffffu, c[nt][e], 4);
-                                const double d1 = __shfl_down_sync(0xffffffffu, c[nt][e], 8);
-                                const double d2 = __shfl_down_sync(0xffffffffu, c[nt][e], 12);
-                                if (lr == 0) {
-                                    const int q = qg + nt * 8 + 2 * lc + e;
-                                    if (on[nt][e]) {
-                                        const double w = we[nt][e];
-                                        const double f = W(fcat, ot, q) * dt;
-                                        tdel[static_cast<size_t>(fcat) * NP + q] -= f * fma(w, d1, c[nt][e]);
-                                        tdel[static_cast<size_t>(pd) * NP + q] += f * fma(w, d2, p2);
-                                    }
-                                }
-                            }
+                        for (int d = 1; d < 8; d <<= 1) {
+                            y1 += __shfl_xor_sync(0xffffffffu, y1, d);
+                            y2 += __shfl_xor_sync(0xffffffffu, y2, d);
+                        }
+                        if (sc0 == 0 && (act[qt] >> cur & 1ull)) {
+                            const double f = W(fcat, ot, qt);
+                            tdel[static_cast<size_t>(fcat) * NP + qt] -= f * y1;
+                            tdel[static_cast<size_t>(pd) * NP + qt] += f * y2;
+                        }
                     }
                 }
+                PROF_MARK(1)
                 // exception cells (non owner-local targets), gathered by the target's owner
                 if (F.nexc > 0) {
                     for (int kind = self ? 1 : 0; kind <= (self ? 1 : 2); kind += self ? 1 : 2) {
@@ -577,22 +717,19 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                                 for (int e = 0; e < 2; ++e) {
                                     const int q = qg + nt * 8 + 2 * lc + e;
                                     const double x = fma(we[nt][e], kd, k5) * W(pa, en.i, q) * W(pb, en.j, q);
-                                    if (on[nt][e]) dadd_cat(D, pd, nt, e, en.coef * x * dt);
+                                    if (on[nt][e]) dadd_cat(D, pd, nt, e, en.coef * x);
                                 }
                         }
-                        if (tail_warp && lr == 0) { // targets in the top row
+                        if (TAIL > 0 && (lane & 7) == 0) { // targets in the top row: the scalar
+                            const int qt = qg + 4 * b + (lane >> 3); // top row's point split
                             const int e2 = __ldg(F.exc_off + kind * (nkr + 1) + ot);
                             const int e3 = __ldg(F.exc_off + kind * (nkr + 1) + ot + 1);
                             for (int ee = e2; ee < e3; ++ee) {
                                 const ExcEntry en = F.exc[ee];
                                 const double k5 = T5[static_cast<size_t>(en.i) * S + en.j];
                                 const double kd = Td[static_cast<size_t>(en.i) * S + en.j];
-                                for (int nt = 0; nt < NT; ++nt)
-                                    for (int e = 0; e < 2; ++e) {
-                                        const int q = qg + nt * 8 + 2 * lc + e;
-                                        const double x = fma(we[nt][e], kd, k5) * W(pa, en.i, q) * W(pb, en.j, q);
-                                        if (on[nt][e]) tdel[static_cast<size_t>(pd) * NP + q] += en.coef * x * dt;
-                                    }
+                                const double x = fma(wts[qt], kd, k5) * W(pa, en.i, qt) * W(pb, en.j, qt);
+                                if (act[qt] >> cur & 1ull) tdel[static_cast<size_t>(pd) * NP + qt] += en.coef * x;
                             }
                         }
                     }
@@ -619,10 +756,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 ++n;
             }
             pbase += n;
+            PROF_MARK(7)
             // ---- Jacobi apply (coalescence.cpp:313-328): every read of `work` for this
             // substep is done, so owners add their register deltas in place, then the
             // cross-block carries and the top row, then the stiffness scan.
             __syncthreads();
+            PROF_MARK(4)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -630,16 +769,17 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     const int q = qg + nt * 8 + 2 * lc + e;
                     const int o = o0 + lr;
 #pragma unroll
-                    for (int c = 0; c < kNCat; ++c) W(c, o, q) += D[c][nt][e];
+                    for (int c = 0; c < kNCat; ++c) W(c, o, q) = fma(dt, D[c][nt][e], W(c, o, q));
                 }
             __syncthreads();
             for (int c = 0; c < kNCat; ++c) // carries into block heads and the top row
                 for (int q = tid; q < NP; q += nthr) {
                     for (int bb = 1; bb < RB; ++bb)
-                        W(c, 8 * bb, q) += carry[(static_cast<size_t>(c) * RB + bb - 1) * NP + q];
+                        W(c, 8 * bb, q) = fma(dt, carry[(static_cast<size_t>(c) * RB + bb - 1) * NP + q], W(c, 8 * bb, q));
                     if (TAIL > 0)
-                        W(c, ot, q) += tdel[static_cast<size_t>(c) * NP + q] +
-                                       carry[(static_cast<size_t>(c) * RB + RB - 1) * NP + q];
+                        W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q] +
+                                                  carry[(static_cast<size_t>(c) * RB + RB - 1) * NP + q],
+                                          W(c, ot, q));
                 }
             __syncthreads();
             for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
@@ -670,7 +810,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             ev_acc += A.kernel_strategy ? ptrip[q] : full_evals;
         }
         __syncthreads();
+        PROF_MARK(5)
     }
+    PROF_FLUSH
     for (int o = 16; o > 0; o >>= 1) {
         tr_acc += __shfl_down_sync(0xffffffffu, tr_acc, o);
         pt_acc += __shfl_down_sync(0xffffffffu, pt_acc, o);
@@ -707,6 +849,11 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
             F.kf[V][b] = T.kf[V][b];
             F.km[V][b] = T.km[V][b];
         }
+    F.std_classes = T.S == 36;
+    for (int V = 0; V < 3; ++V)
+        for (int b = 0; b < kDmmaRB; ++b)
+            F.std_classes = F.std_classes && T.kf[V][b] == 2 * b && T.km[V][b] == 2 * b + 2;
+    if (const char *ev = std::getenv("FSBM_DMMA_UNROLL"); ev && ev[0] == '0') F.std_classes = 0; // A/B
     F.nbatches = (A.nactive_host + kDmmaNP - 1) / kDmmaNP;
     F.blob = T.blob;
     F.gains = T.gains;
@@ -719,7 +866,31 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
         return 6;
     }
     const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
+#ifdef FSBM_DMMA_PROF
+    static unsigned long long *dprof = nullptr;
+    if (!dprof) {
+        cudaMalloc(&dprof, 12 * 8 * 8);
+        cudaMemset(dprof, 0, 12 * 8 * 8);
+    }
+    F.prof = dprof;
+#endif
     coal_dmma_kernel<<<grid, kDmmaThreads, smem, s>>>(A, F);
+#ifdef FSBM_DMMA_PROF
+    {
+        unsigned long long h[96];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost);
+        static int calls = 0;
+        if (++calls % 4 == 0) {
+            fprintf(stderr, "dmma prof (Gcycles per warp, all CTAs): setup tail wait kloops barrier rest emit other\n");
+            for (int w = 0; w < 12; ++w) {
+                fprintf(stderr, "  w%2d b%d:", w, (w % 4 + w / 4) % 4);
+                for (int k = 0; k < 8; ++k) fprintf(stderr, " %7.2f", h[w * 8 + k] / 1e9);
+                fprintf(stderr, "\n");
+            }
+        }
+    }
+#endif
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fast_err() = std::string("dmma path launch: ") + cudaGetErrorString(e);

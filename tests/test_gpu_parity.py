@@ -17,8 +17,8 @@ RTOL = 1e-12
 ATOL_FRAC = 1e-15
 
 
-def make_ctx(nkr, pair_scale_step=0.05, coeff=1.0, family="golovin", pairs=None):
-    r = fsbm.equal_range_ratio(nkr)
+def make_ctx(nkr, pair_scale_step=0.05, coeff=1.0, family="golovin", pairs=None, ratio=None):
+    r = ratio or fsbm.equal_range_ratio(nkr)
     grid = fsbm.make_mass_grid(nkr, 3.35e-14, r)
     pairs = pairs or fsbm.default_pair_registry()
     tabs = fsbm.build_tables(grid, pairs, fsbm.KernelParams(family, coeff, 1.5, pair_scale_step))
@@ -319,3 +319,30 @@ def test_device_generator_and_conservation_at_scale(oracle):
         b = np.ascontiguousarray(B0[:, p])
         assert oracle.coal_step(x, abd, t750, t500, g, b, float(P[p]))[0] == 0
         assert_close(B1[:, p], b, f"point {p}")
+
+
+@pytest.mark.parametrize("nkr,ratio,pmode", [
+    (33, None, "levels"),     # level pressure, groups straddling levels: 1-2 slots per batch
+    (33, None, "random"),     # per-point pressure: general (K500 + w*Kd as a K=72 GEMM)
+    (33, 1.7, "random"),      # non-doubling grid: exception (non owner-local) cells
+    (33, 2.2, "levels"),
+    (32, None, "levels"),     # no top-row tile
+    (32, 1.9, "random"),
+])
+def test_fast_pressure_fields_and_grids(oracle, nkr, ratio, pmode):
+    """FAST path against the oracle on every point of a multi-batch grid, for uniform,
+    mixed and per-point pressure weights and for grids with exception cells."""
+    ctx, grid, tabs = make_ctx(nkr, ratio=ratio)
+    st, mask, B = thunder_host(oracle, ctx, 5, 7, 37, 0.9, 5)
+    if pmode == "random":
+        rng = np.random.default_rng(11)
+        st.pressure[:] = rng.uniform(350.0, 950.0, st.pressure.shape)
+        st.pressure[::7] = 600.0  # some exact repeats
+    s, cnt_o, _, Bo = run_oracle_grid(oracle, ctx, tabs, st, mask, B, dt=0.3)
+    assert s == 0
+    dst = device_state(st)
+    cnt = fsbm.WorkCounters()
+    fsbm.fissioned_step(dst, None, fsbm.StepContext(ctx, fsbm.CoalConfig(0.3, 1), cnt), fsbm.ExecPlan())
+    got = np.stack([b.cpu().numpy().reshape(-1, nkr) for b in dst.bins])
+    assert_close(got, Bo, f"nkr{nkr} ratio{ratio} {pmode}")
+    assert [cnt.triples, cnt.points, cnt.kernel_evals] == [int(v) for v in cnt_o]
