@@ -441,16 +441,30 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             ptrip[q] = 0;
         }
         __syncthreads();
-        for (int k = wid; k < S; k += NW) // q across lanes: conflict-free STS; 6 loads in flight
-            for (int q = lane; q < NP; q += 32) {
-                const uint32_t p = pidx[q];
-                const bool ok = p != 0xffffffffu && k < nkr;
-                double v[kNCat];
+        { // spectra -> work: all loads of a thread issued before its stores (q across lanes)
+            constexpr int KR = (36 + kDmmaThreads / 32 - 1) / (kDmmaThreads / 32), QR = (NP + 31) / 32;
+            double v[KR][QR][kNCat];
 #pragma unroll
-                for (int c = 0; c < kNCat; ++c) v[c] = ok ? __ldg(A.bins[c] + static_cast<size_t>(p) * nkr + k) : 0.0;
+            for (int kk = 0; kk < KR; ++kk)
 #pragma unroll
-                for (int c = 0; c < kNCat; ++c) W(c, k, q) = v[c];
-            }
+                for (int qq = 0; qq < QR; ++qq) {
+                    const int k = wid + kk * NW, q = lane + 32 * qq;
+                    const uint32_t p = q < NP ? pidx[q] : 0xffffffffu;
+                    const bool ok = p != 0xffffffffu && k < nkr;
+#pragma unroll
+                    for (int c = 0; c < kNCat; ++c)
+                        v[kk][qq][c] = ok ? __ldg(A.bins[c] + static_cast<size_t>(p) * nkr + k) : 0.0;
+                }
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int qq = 0; qq < QR; ++qq) {
+                    const int k = wid + kk * NW, q = lane + 32 * qq;
+                    if (k < S && q < NP)
+#pragma unroll
+                        for (int c = 0; c < kNCat; ++c) W(c, k, q) = v[kk][qq][c];
+                }
+        }
         if (!gains_ready) {
             mbar_wait(&mbar[NBUF], 0);
             gains_ready = true;
