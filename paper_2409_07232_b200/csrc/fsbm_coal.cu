@@ -722,8 +722,10 @@ int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NC
     }
     // Pipeline over i-chunks: H2D (s_in) -> flags/compaction/kernel (stream) -> D2H
     // (s_out), kSlots chunks in flight; pinned host memory makes the copies async.
-    const int nchunks = std::max(1, std::min(g.ni, 8));
-    const int rows = (g.ni + nchunks - 1) / nchunks;
+    // ~192 MB chunks: pipeline fill (first H2D) and drain (last kernel + D2H) stay a few
+    // percent of the step while the copy engines run H2D and D2H concurrently.
+    const size_t row_bytes = per_i * (FSBM_NCAT * static_cast<size_t>(nkr) * sizeof(double) + 17);
+    const int rows = static_cast<int>(std::max<size_t>(1, std::min<size_t>(g.ni, (192u << 20) / row_bytes)));
     const size_t chunk_np = static_cast<size_t>(rows) * per_i;
     const size_t need = FSBM_NCAT * chunk_np * nkr * sizeof(double) + 2 * chunk_np * sizeof(double) +
                         chunk_np + 256;
