@@ -337,6 +337,13 @@ def run_ours(args):
         roof["hbm_frac_of_measured"] = hbm_gbs / peaks["hbm_gbs"]
     except Exception:
         pass
+    try:  # DRAM bytes of the coal kernel from the committed ncu --set full capture, per launch
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        if tr["nkr"] == nkr:
+            roof["traffic"] = tr["bytes_per_update"] * (cnt.points / args.steps)
+            roof["traffic_source"] = tr["source"]
+    except Exception:
+        pass
 
     # ---- e2e through the host C ABI ----
     e2e = None
