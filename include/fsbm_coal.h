@@ -171,6 +171,43 @@ int fsbm_ctx_last_timing(const fsbm_ctx *ctx, float *coal_kernel_ms, int *launch
  * the denominator of its FP64 roofline live with this. */
 int fsbm_probe_fp64_peak(int device, double *tflops);
 
+/* ---- state snapshots and the digit-agreement comparator ---- */
+
+/* write_snapshot (snapshot.hpp:8-17, snapshot.cpp:46-73): the CBSNAP01 layout
+ * (magic, u32 version 1, u32 nkr, i32 ids..jde, f64 ratio, u32 ncat + names,
+ * f64 x[nkr], temperature[np], pressure[np], 6 x bins[np*nkr]), little-endian,
+ * bit-exact on round trip.  Host arrays in GridState layout. */
+int fsbm_snapshot_write(const char *path, fsbm_ranges ranges, int nkr, double ratio,
+                        const double *x, const double *temperature, const double *pressure,
+                        const double *const bins[FSBM_NCAT]);
+
+/* read_snapshot (snapshot.cpp:75-135) in two calls: the header, then the arrays into
+ * caller buffers sized from it.  FSBM_CONFIG (ConfigError) on a malformed, truncated or
+ * over-long file, with the reference's messages and check order. */
+int fsbm_snapshot_read_header(const char *path, fsbm_ranges *ranges, int *nkr, double *ratio);
+int fsbm_snapshot_read(const char *path, double *x, double *temperature, double *pressure,
+                       double *const bins[FSBM_NCAT]);
+
+/* FieldDiff (verify.hpp:20-26). */
+typedef struct {
+    int min_digits;
+    double mean_digits;
+    uint64_t count_compared;
+    uint64_t count_exact;
+} fsbm_field_diff;
+
+/* compare_states (verify.cpp:65-80) on DEVICE arrays of two states of the same shape
+ * (the caller checks ranges/nkr -> ShapeError): out[9] = mass_grid, temperature,
+ * pressure, liquid..graupel, each the digit_agreement (verify.cpp:12-26) min / mean /
+ * exact count over its values, one reduction launch.  FSBM_DOMAIN on a non-finite
+ * value (digit_agreement throws DomainError). */
+int fsbm_compare_states_device(int device, size_t npoints, int nkr, const double *x_a,
+                               const double *temperature_a, const double *pressure_a,
+                               const double *const bins_a[FSBM_NCAT], const double *x_b,
+                               const double *temperature_b, const double *pressure_b,
+                               const double *const bins_b[FSBM_NCAT], fsbm_field_diff *out,
+                               void *stream);
+
 #ifdef __cplusplus
 }
 #endif

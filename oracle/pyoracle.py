@@ -210,6 +210,13 @@ class Reference:
                                            C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp,
                                            _dp]
         L.cbref_fission_predicates.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _u8p, _u64p]
+        for name in ("cbref_write_snapshot", "cbref_read_snapshot", "cbref_compare_states"):
+            getattr(L, name).restype = C.c_int
+        L.cbref_write_snapshot.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_double,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.cbref_read_snapshot.argtypes = [C.c_char_p] + [C.c_void_p] * 7
+        L.cbref_compare_states.argtypes = [C.c_void_p] + [C.c_int] + [C.c_void_p] * 12
+        L.cbref_digit_agreement.argtypes = [C.c_double, C.c_double, C.c_void_p]
         L.cbref_fissioned_step.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                            C.c_double, C.c_int, C.c_void_p, _dp, _dp, _dp, _dp,
                                            _dp, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -319,3 +326,47 @@ class Reference:
                                            threads, kernel_strategy, scratch_strategy, n_patches,
                                            n_tiles, cnt, tim, err)
         return st, cnt, tim, err
+
+    # ---- snapshot.cpp / verify.cpp (reference state I/O and comparator) ----
+    def write_snapshot(self, path, ranges, x, ratio, T, P, bins):
+        """bins: (6, npoints*nkr) or (6, npoints, nkr)."""
+        L = self.lib
+        rg = np.ascontiguousarray(ranges, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        st = L.cbref_write_snapshot(str(path).encode(), rg.ctypes.data, len(x), C.c_double(ratio),
+                                    x.ctypes.data, np.ascontiguousarray(T).ctypes.data,
+                                    np.ascontiguousarray(P).ctypes.data,
+                                    np.ascontiguousarray(bins, np.float64).ctypes.data)
+        return st
+
+    def read_snapshot(self, path):
+        """Returns (status, ranges[6], x, ratio, T, P, bins (6, np*nkr))."""
+        L = self.lib
+        rg = np.zeros(6, np.int32)
+        nkr, ratio = C.c_int(), C.c_double()
+        st = L.cbref_read_snapshot(str(path).encode(), rg.ctypes.data, C.byref(nkr), C.byref(ratio),
+                                   None, None, None, None)
+        if st:
+            return st, None, None, None, None, None, None
+        np_ = int((rg[1] - rg[0] + 1) * (rg[3] - rg[2] + 1) * (rg[5] - rg[4] + 1))
+        x, T, P = np.zeros(nkr.value), np.zeros(np_), np.zeros(np_)
+        bins = np.zeros((NCAT, np_ * nkr.value))
+        st = L.cbref_read_snapshot(str(path).encode(), rg.ctypes.data, C.byref(nkr), C.byref(ratio),
+                                   x.ctypes.data, T.ctypes.data, P.ctypes.data, bins.ctypes.data)
+        return st, rg, x, ratio.value, T, P, bins
+
+    def digit_agreement(self, a, b):
+        d = C.c_int()
+        st = self.lib.cbref_digit_agreement(C.c_double(a), C.c_double(b), C.byref(d))
+        return st, d.value
+
+    def compare_states(self, ranges, xa, Ta, Pa, binsa, xb, Tb, Pb, binsb):
+        """Per field (9): (min_digits, mean_digits, count_compared, count_exact)."""
+        rg = np.ascontiguousarray(ranges, np.int32)
+        mn, mean = np.zeros(9, np.int32), np.zeros(9)
+        cmp_, ex = np.zeros(9, np.uint64), np.zeros(9, np.uint64)
+        c = lambda a: np.ascontiguousarray(a, np.float64).ctypes.data
+        st = self.lib.cbref_compare_states(rg.ctypes.data, len(xa), c(xa), c(Ta), c(Pa), c(binsa),
+                                           c(xb), c(Tb), c(Pb), c(binsb), mn.ctypes.data,
+                                           mean.ctypes.data, cmp_.ctypes.data, ex.ctypes.data)
+        return st, [(int(mn[f]), float(mean[f]), int(cmp_[f]), int(ex[f])) for f in range(9)]

@@ -1,7 +1,7 @@
 // ref_shim.cpp -- TEST INFRASTRUCTURE ONLY (oracle side).
 //
 // A thin extern "C" shim over the *unmodified* reference library
-// (/root/reference/proj/src/{mass_grid,kernels,coalescence,driver}.cpp),
+// (/root/reference/proj/src/{mass_grid,kernels,coalescence,driver,snapshot,verify}.cpp),
 // compiled by oracle/Makefile into oracle/_ref/libcoalbench_ref.so.  It lets
 // the parity tests and bench.py's CPU-baseline leg call the real reference
 // (`coal_step`, `fissioned_step`, `GainTable`, `build_tables`, ...) on the
@@ -22,6 +22,8 @@
 #include "coalbench/errors.hpp"
 #include "coalbench/kernels.hpp"
 #include "coalbench/mass_grid.hpp"
+#include "coalbench/snapshot.hpp"
+#include "coalbench/verify.hpp"
 
 using namespace coalbench;
 
@@ -330,6 +332,89 @@ int cbref_fissioned_step(int ni, int nk, int nj, int nkr, double x1, double rati
             timings_out[1] = pt.step_s;
         }
         return st;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+namespace {
+GridState state_from(const int* rg, int nkr, double ratio, const double* x, const double* T,
+                     const double* P, const double* bins) {
+    GridState s;
+    s.ranges = Ranges{rg[0], rg[1], rg[2], rg[3], rg[4], rg[5]};
+    s.grid.x.assign(x, x + nkr);
+    s.grid.ratio = ratio;
+    const std::size_t np = s.ranges.npoints();
+    s.temperature.assign(T, T + np);
+    s.pressure.assign(P, P + np);
+    for (int c = 0; c < kNumCategories; ++c)
+        s.bins[c].assign(bins + static_cast<std::size_t>(c) * np * nkr,
+                         bins + static_cast<std::size_t>(c + 1) * np * nkr);
+    return s;
+}
+} // namespace
+
+/// write_snapshot of a state given as ranges[6], x[nkr], T/P[np], bins[6*np*nkr].
+int cbref_write_snapshot(const char* path, const int* ranges, int nkr, double ratio,
+                         const double* x, const double* T, const double* P, const double* bins) {
+    try {
+        write_snapshot(state_from(ranges, nkr, ratio, x, T, P, bins), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+/// read_snapshot: call with bins == nullptr to get ranges[6]/nkr/ratio only.
+int cbref_read_snapshot(const char* path, int* ranges, int* nkr, double* ratio, double* x,
+                        double* T, double* P, double* bins) {
+    try {
+        GridState s = read_snapshot(path);
+        const Ranges& r = s.ranges;
+        const int rv[6] = {r.ids, r.ide, r.kds, r.kde, r.jds, r.jde};
+        std::memcpy(ranges, rv, sizeof(rv));
+        *nkr = s.nkr();
+        *ratio = s.grid.ratio;
+        if (bins) {
+            const std::size_t np = r.npoints();
+            std::memcpy(x, s.grid.x.data(), sizeof(double) * s.nkr());
+            std::memcpy(T, s.temperature.data(), sizeof(double) * np);
+            std::memcpy(P, s.pressure.data(), sizeof(double) * np);
+            for (int c = 0; c < kNumCategories; ++c)
+                std::memcpy(bins + static_cast<std::size_t>(c) * np * s.nkr(), s.bins[c].data(),
+                            sizeof(double) * np * s.nkr());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int cbref_digit_agreement(double a, double b, int* digits) {
+    try {
+        *digits = digit_agreement(a, b);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+/// compare_states over two states of the same ranges/nkr; per field (9, the
+/// reference's order): min_digits, mean_digits, count_compared, count_exact.
+int cbref_compare_states(const int* ranges, int nkr, const double* xa, const double* Ta,
+                         const double* Pa, const double* binsa, const double* xb,
+                         const double* Tb, const double* Pb, const double* binsb, int* min_d,
+                         double* mean_d, uint64_t* compared, uint64_t* exact) {
+    try {
+        DiffReport r = compare_states(state_from(ranges, nkr, 2.0, xa, Ta, Pa, binsa),
+                                      state_from(ranges, nkr, 2.0, xb, Tb, Pb, binsb));
+        for (std::size_t f = 0; f < r.fields.size(); ++f) {
+            min_d[f] = r.fields[f].min_digits;
+            mean_d[f] = r.fields[f].mean_digits;
+            compared[f] = r.fields[f].count_compared;
+            exact[f] = r.fields[f].count_exact;
+        }
+        return 0;
     } catch (const std::exception& e) {
         return status_of(e);
     }

@@ -5,5 +5,6 @@ include/fsbm_coal.h); ``coalbench`` mirrors the reference's host interface.
 """
 from . import _lib
 from .coalbench import *  # noqa: F401,F403
+from .verify import *  # noqa: F401,F403
 
 __version__ = "0.1.0"

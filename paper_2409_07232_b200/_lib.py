@@ -40,6 +40,11 @@ class fsbm_error(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("category", "bin", "has_point", "i", "k", "j")]
 
 
+class fsbm_field_diff(C.Structure):
+    _fields_ = [("min_digits", C.c_int), ("mean_digits", C.c_double),
+                ("count_compared", C.c_uint64), ("count_exact", C.c_uint64)]
+
+
 _vp = C.c_void_p
 _SIGS = {
     "fsbm_last_error": ([], C.c_char_p),
@@ -64,6 +69,14 @@ _SIGS = {
                                         _vp * NCAT, _vp], C.c_int),
     "fsbm_ctx_last_timing": ([_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
     "fsbm_probe_fp64_peak": ([C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "fsbm_snapshot_write": ([C.c_char_p, fsbm_ranges, C.c_int, C.c_double, _vp, _vp, _vp,
+                             _vp * NCAT], C.c_int),
+    "fsbm_snapshot_read_header": ([C.c_char_p, C.POINTER(fsbm_ranges), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_double)], C.c_int),
+    "fsbm_snapshot_read": ([C.c_char_p, _vp, _vp, _vp, _vp * NCAT], C.c_int),
+    "fsbm_compare_states_device": ([C.c_int, C.c_size_t, C.c_int, _vp, _vp, _vp, _vp * NCAT,
+                                    _vp, _vp, _vp, _vp * NCAT, C.POINTER(fsbm_field_diff), _vp],
+                                   C.c_int),
 }
 
 _lib = None

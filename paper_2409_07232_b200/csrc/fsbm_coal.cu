@@ -926,3 +926,5 @@ int fsbm_ctx_last_timing(const fsbm_ctx *c, float *coal_kernel_ms, int *launches
 }
 
 } // extern "C"
+
+#include "state_io.cuh"
