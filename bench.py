@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--nj", type=int, default=CONFIG["nj"])
     ap.add_argument("--nk", type=int, default=CONFIG["nk"])
     ap.add_argument("--cf", type=float, default=CONFIG["cloud_fraction"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

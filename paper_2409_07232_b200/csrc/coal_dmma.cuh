@@ -393,6 +393,13 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + NBUF + 1);        // [NP]
     int *pfail = reinterpret_cast<int *>(pidx + NP);                       // [NP]
     __shared__ unsigned long long cta_act;
+    // per point group and category: last bin holding a non-zero value at any live point.
+    // Products with an exactly-zero spectrum value vanish (the reference skips rate == 0
+    // triples, coalescence.cpp:286-292): a pass whose owner rows are all zero, or whose
+    // streamed spectrum is zero, is skipped; the generic (two-half) K-loops also stop at
+    // the streamed spectrum's last non-zero bin.  (Cutting K-steps inside the unrolled
+    // loops measured slower: the early exits break the schedule.)
+    __shared__ int kzg[kDmmaG][kNCat];
     __shared__ int relcnt[kDmmaNBUF];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
@@ -474,13 +481,15 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
         for (int sub = 0; sub < A.substeps; ++sub) {
             if (tid == 0) cta_act = 0ull;
             for (int f = tid; f < kNCat * (RB + 1) * NP; f += nthr) carry[f] = 0.0; // carry + tdel
+            if (tid < kDmmaG * kNCat) kzg[tid / kNCat][tid % kNCat] = -1;
             __syncthreads();
             for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
                 unsigned nz = 0;
-                for (int c = 0; c < kNCat; ++c) {
-                    bool any = false;
-                    for (int k = 0; k < nkr && !any; ++k) any = W(c, k, q) != 0.0;
-                    nz |= any ? (1u << c) : 0u;
+                for (int c = 0; c < kNCat; ++c) { // scanned from the top: last non-zero bin
+                    int l = nkr - 1;
+                    while (l >= 0 && W(c, l, q) == 0.0) --l;
+                    nz |= l >= 0 ? (1u << c) : 0u;
+                    if (l >= 0 && pfail[q] == 0) atomicMax(&kzg[q / (NT * 8)][c], l);
                 }
                 unsigned long long m = 0, trip = 0;
                 for (int pp = 0; pp < npairs; ++pp)
@@ -573,6 +582,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     const int astride = X == 0 ? 4 : 4 * S;             // per K-step
                     const int abase = X == 0 ? o * S + lc : lc * S + o; // at ks = 0
                     const int kf = F.kf[V][b], km = F.km[V][b];
+                    const int kzf = kzg[g][fcat], kzs = kzg[g][X == 0 ? pb : pa];
+                    const int kend = (kzs >> 2) + 1; // K-steps that can see a non-zero B
+                    if (o0 <= kzf && kzs >= 0) {     // else every product of this block is zero
                     double Y1[NT][2], Y2[NT][2], YG[NT][2];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
@@ -617,7 +629,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             c1[nt][0] = c1[nt][1] = c2[nt][0] = c2[nt][1] = 0.0;
                         int ai = abase;
 #pragma unroll 2
-                        for (int ks = 0; ks < kf; ++ks, ai += astride) { // every cell owned-far
+                        for (int ks = 0; ks < min(kf, kend); ++ks, ai += astride) { // every cell owned-far
                             const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
                             const double t2 = t * Glo[ai];
 #pragma unroll
@@ -632,7 +644,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             cg[nt][0] = c1[nt][0];
                             cg[nt][1] = c1[nt][1];
                         }
-                        for (int ks = kf; ks < km; ++ks, ai += astride) { // diagonal steps
+                        for (int ks = kf; ks < min(km, kend); ++ks, ai += astride) { // diagonal steps
                             const int s = 4 * ks + lc;
                             const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
                             // gain view: R-cross s<o, R-self s<o (+ s==o at 1/2), C s<=o
@@ -650,7 +662,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             }
                         }
 #pragma unroll 2
-                        for (int ks = km; ks < KS; ++ks, ai += astride) { // no owned gains
+                        for (int ks = km; ks < min(KS, kend); ++ks, ai += astride) { // no owned gains
                             const double t = summed ? fma(wu, Td[ai], T5[ai]) : Ta[ai];
 #pragma unroll
                             for (int nt = 0; nt < NT; ++nt) {
@@ -686,15 +698,16 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     emit_switch(fcat * kNCat + pd, D, L, Gn);
 
                     PROF_MARK(6)
+                    } // non-zero block
                     // the top row (bin nkr-1, nkr % 8 == 1): a 1-row GEMM is 1/8 of a DMMA tile, so
                     // it runs on the FP64 CUDA cores, balanced over the group's four warps:
                     // warp b takes points 4b..4b+3 of the group, 8 lanes per point split s.
-                    if (TAIL > 0) {
+                    if (TAIL > 0 && kzf >= ot && kzs >= 0) { // top bin non-zero somewhere
                         const int qt = qg + 4 * b + (lane >> 3), sc0 = lane & 7;
                         const double wq = wts[qt];
                         const double *vt = &W(X == 0 ? pb : pa, 0, qt);
                         double y1 = 0.0, y2 = 0.0;
-                        for (int sx = sc0; sx < nkr; sx += 8) {
+                        for (int sx = sc0; sx <= kzs; sx += 8) {
                             const int ti = X == 0 ? ot * S + sx : sx * S + ot;
                             const double m = V == 2 ? (sx <= ot ? 1.0 : 0.0)
                                                     : (sx < ot ? 1.0 : (V == 1 && sx == ot ? 0.5 : 0.0));
