@@ -594,21 +594,15 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     if (unrolled) { // fully unrolled K-loops (the common case)
                         double c1[NT][2] = {}, c2[NT][2], cg[NT][2];
 #define FSBM_PASS(BB, IN)                                                                          \
-    dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN>(T5, Td, wu, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg)
-                        if (wmode == 1) {
-                            switch (b) {
-                            case 0: FSBM_PASS(0, true); break;
-                            case 1: FSBM_PASS(1, true); break;
-                            case 2: FSBM_PASS(2, true); break;
-                            default: FSBM_PASS(3, true); break;
-                            }
-                        } else {
-                            switch (b) {
-                            case 0: FSBM_PASS(0, false); break;
-                            case 1: FSBM_PASS(1, false); break;
-                            case 2: FSBM_PASS(2, false); break;
-                            default: FSBM_PASS(3, false); break;
-                            }
+    dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg)
+                        // one instantiation per block (K500 + w*Kd with w = 0 for p <= 500 hPa):
+                        // halving the unrolled code keeps the kernel inside the instruction cache
+                        const double wi = wmode == 1 ? wu : 0.0;
+                        switch (b) {
+                        case 0: FSBM_PASS(0, true); break;
+                        case 1: FSBM_PASS(1, true); break;
+                        case 2: FSBM_PASS(2, true); break;
+                        default: FSBM_PASS(3, true); break;
                         }
 #undef FSBM_PASS
 #pragma unroll
