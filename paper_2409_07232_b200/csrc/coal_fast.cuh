@@ -199,6 +199,10 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     unsigned long long *ptrip = act + F.npts;                    // [npts]
     uint32_t *pidx = reinterpret_cast<uint32_t *>(ptrip + F.npts); // [npts]
     int *pfail = reinterpret_cast<int *>(pidx + F.npts);         // [npts]
+    // last non-zero bin per (point, category): products with an exactly-zero spectrum value
+    // vanish (the reference skips rate == 0 triples, coalescence.cpp:286-292), so a row's
+    // stream loop stops there and a row whose owner values are zero skips its emission
+    short *lz = reinterpret_cast<short *>(pfail + F.npts);        // [npts][6]
     __shared__ unsigned long long cta_act;
 
     auto IX = [&](int s, int c, int k, int q) -> size_t {
@@ -253,10 +257,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
             for (int q = tid; q < F.npts; q += nthr) {
                 const int s = q / PTS, qq = q % PTS;
                 unsigned nz = 0;
-                for (int c = 0; c < kNCat; ++c) {
-                    bool any = false;
-                    for (int k = 0; k < nkr && !any; ++k) any = work[IX(s, c, k, qq)] != 0.0;
-                    nz |= any ? (1u << c) : 0u;
+                for (int c = 0; c < kNCat; ++c) { // scanned from the top: last non-zero bin
+                    int l = nkr - 1;
+                    while (l >= 0 && work[IX(s, c, l, qq)] == 0.0) --l;
+                    nz |= l >= 0 ? (1u << c) : 0u;
+                    lz[q * kNCat + c] = static_cast<short>(l);
                 }
                 unsigned long long m = 0;
                 unsigned long long trip = 0;
@@ -295,9 +300,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
                     // row pass (owner row r, stream nb[t]) and column pass (owner col r, stream na[t])
                     double accR0 = 0, accR1 = 0, alR0 = 0, alR1 = 0, ahR0 = 0, ahR1 = 0;
                     double accC0 = 0, accC1 = 0, alC0 = 0, alC1 = 0, ahC0 = 0, ahC1 = 0;
-                    if (self) {
+                    const double2 nar = *reinterpret_cast<const double2 *>(na + static_cast<size_t>(r) * PTS);
+                    const double2 nbr = *reinterpret_cast<const double2 *>(nb + static_cast<size_t>(r) * PTS);
+                    const short *l0 = lz + (s * PTS + q0) * kNCat, *l1 = l0 + kNCat;
+                    // stream bins past the last non-zero one contribute nothing
+                    const int tend = 1 + max(max(l0[a], l0[b]), max(l1[a], l1[b]));
+                    const bool live_row = nar.x != 0.0 || nar.y != 0.0 || (!self && (nbr.x != 0.0 || nbr.y != 0.0));
+                    if (!live_row) {
+                        // every owner term of this row is zero; exceptions below still run
+                    } else if (self) {
 #pragma unroll 4
-                        for (int t = 0; t < nkr; ++t) {
+                        for (int t = 0; t < tend; ++t) {
                             const double2 kk = __ldg(TRp + static_cast<size_t>(t) * nkr + r);
                             const double2 gc = __ldg(F.GR + static_cast<size_t>(t) * nkr + r);
                             const double2 sv = *reinterpret_cast<const double2 *>(nb + static_cast<size_t>(t) * PTS);
@@ -312,7 +325,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
                         }
                     } else {
 #pragma unroll 2
-                        for (int t = 0; t < nkr; ++t) {
+                        for (int t = 0; t < tend; ++t) {
                             const double2 kr = __ldg(TRp + static_cast<size_t>(t) * nkr + r);
                             const double2 gr = __ldg(F.GR + static_cast<size_t>(t) * nkr + r);
                             const double2 kc = __ldg(TCp + static_cast<size_t>(t) * nkr + r);
@@ -338,8 +351,6 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
                         }
                     }
                     // ---- owner emission: delta[*][r] (owner r), dhi[d][r+1] (owner r) ----
-                    const double2 nar = *reinterpret_cast<const double2 *>(na + static_cast<size_t>(r) * PTS);
-                    const double2 nbr = *reinterpret_cast<const double2 *>(nb + static_cast<size_t>(r) * PTS);
                     const double fR0 = nar.x * A.dt_sub, fR1 = nar.y * A.dt_sub;
                     double *dA = delta + IX(s, a, r, q0);
                     double *dD = delta + IX(s, d, r, q0);
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
 inline size_t fast_smem_bytes(int nkr, int nsets, int pts) {
     const size_t arr = static_cast<size_t>(nsets) * kNCat * nkr * pts;
     const size_t npts = static_cast<size_t>(nsets) * pts;
-    return 3 * arr * sizeof(double) + npts * (sizeof(double) + 8 + 8 + 4 + 4);
+    return 3 * arr * sizeof(double) + npts * (sizeof(double) + 8 + 8 + 4 + 4 + kNCat * sizeof(short));
 }
 
 template <int R>
