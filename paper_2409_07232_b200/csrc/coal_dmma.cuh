@@ -405,6 +405,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
     const int wid = tid >> 5, lane = tid & 31;
     // block b of group g, rotated by g so every SMSP (wid % 4) hosts a mix of blocks
+    // block rotated by group so every SMSP (wid % 4) hosts three different blocks: measured
+    // better than one block per SMSP (instruction-cache friendly, unbalanced) or the pairing
+    // {s, 3-s} per SMSP
     const int g = wid / RB, b = (wid % RB + g) % RB;
     const int o0 = 8 * b;
     const int lr = lane >> 2, lc = lane & 3;
