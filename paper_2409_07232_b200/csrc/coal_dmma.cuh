@@ -451,29 +451,26 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             ptrip[q] = 0;
         }
         __syncthreads();
-        { // spectra -> work: all loads of a thread issued before its stores (q across lanes)
-            constexpr int KR = (36 + kDmmaThreads / 32 - 1) / (kDmmaThreads / 32), QR = (NP + 31) / 32;
-            double v[KR][QR][kNCat];
+        { // spectra -> work, coalesced: a warp instruction covers 4 points x 8 consecutive bins
+          // (64-byte runs of each point's spectrum); quads of (category, 4 points) per warp
+            constexpr int NQ = kNCat * NP / 4; // 72 quads
+            const int qs = lane >> 3, kc = lane & 7;
+            for (int u = wid; u < NQ; u += NW) {
+                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+                const uint32_t p = pidx[q];
+                const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
+                double v[5];
 #pragma unroll
-            for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                for (int qq = 0; qq < QR; ++qq) {
-                    const int k = wid + kk * NW, q = lane + 32 * qq;
-                    const uint32_t p = q < NP ? pidx[q] : 0xffffffffu;
-                    const bool ok = p != 0xffffffffu && k < nkr;
-#pragma unroll
-                    for (int c = 0; c < kNCat; ++c)
-                        v[kk][qq][c] = ok ? __ldg(A.bins[c] + static_cast<size_t>(p) * nkr + k) : 0.0;
+                for (int jj = 0; jj < 5; ++jj) {
+                    const int k = kc + 8 * jj;
+                    v[jj] = p != 0xffffffffu && k < nkr ? __ldg(src + k) : 0.0;
                 }
 #pragma unroll
-            for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                for (int qq = 0; qq < QR; ++qq) {
-                    const int k = wid + kk * NW, q = lane + 32 * qq;
-                    if (k < S && q < NP)
-#pragma unroll
-                        for (int c = 0; c < kNCat; ++c) W(c, k, q) = v[kk][qq][c];
+                for (int jj = 0; jj < 5; ++jj) {
+                    const int k = kc + 8 * jj;
+                    if (k < S) W(c, k, q) = v[jj];
                 }
+            }
         }
         if (!gains_ready) {
             mbar_wait(&mbar[NBUF], 0);
@@ -821,12 +818,21 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 if (pfail[q] == 2) pfail[q] = 3;
         }
         // ---- write back + counters ----
-        for (int c = 0; c < kNCat; ++c)
-            for (int k = wid; k < nkr; k += NW)
-                for (int q = lane; q < NP; q += 32) {
-                    const uint32_t p = pidx[q];
-                    if (p != 0xffffffffu) A.bins[c][static_cast<size_t>(p) * nkr + k] = W(c, k, q);
+        {
+            constexpr int NQ = kNCat * NP / 4;
+            const int qs = lane >> 3, kc = lane & 7;
+            for (int u = wid; u < NQ; u += NW) {
+                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+                const uint32_t p = pidx[q];
+                if (p == 0xffffffffu) continue;
+                double *dst = A.bins[c] + static_cast<size_t>(p) * nkr;
+#pragma unroll
+                for (int jj = 0; jj < 5; ++jj) {
+                    const int k = kc + 8 * jj;
+                    if (k < nkr) dst[k] = W(c, k, q);
                 }
+            }
+        }
         for (int q = tid; q < NP; q += nthr) {
             if (pidx[q] == 0xffffffffu || pfail[q] != 0) continue;
             tr_acc += ptrip[q];
