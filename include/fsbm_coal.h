@@ -165,6 +165,12 @@ int fsbm_synth_thunderstorm_device(fsbm_ctx *ctx, size_t npoints, uint64_t point
  * the number of this library's kernels that call launched. */
 int fsbm_ctx_last_timing(const fsbm_ctx *ctx, float *coal_kernel_ms, int *launches);
 
+/* Which FSBM_NUMERICS_FAST kernel this context dispatches to: 1 coal_fast (direct
+ * FP64, any nkr), 2 coal_dmma (FP64 tensor cores, nkr 32/33), 3 coal_dmmag (FP64
+ * tensor cores, general band grids up to 96 bins).  FSBM_FAST_KERNEL=direct|dmma|dmmag
+ * in the environment at fsbm_ctx_create forces one (A/B and parity testing). */
+int fsbm_ctx_fast_kernel(const fsbm_ctx *ctx, int *kernel);
+
 /* Measured FP64 roof of `device`: a DFMA-chain microbenchmark (8 independent
  * chains per thread, full occupancy) timed with CUDA events; FLOP/s counts 2 per
  * DFMA.  MEASURED_PEAKS.json carries HBM and bf16 only, so the bench measures

@@ -68,6 +68,7 @@ _SIGS = {
     "fsbm_synth_thunderstorm_device": ([_vp, C.c_size_t, C.c_uint64, _vp, C.c_uint64,
                                         _vp * NCAT, _vp], C.c_int),
     "fsbm_ctx_last_timing": ([_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
+    "fsbm_ctx_fast_kernel": ([_vp, C.POINTER(C.c_int)], C.c_int),
     "fsbm_probe_fp64_peak": ([C.c_int, C.POINTER(C.c_double)], C.c_int),
     "fsbm_snapshot_write": ([C.c_char_p, fsbm_ranges, C.c_int, C.c_double, _vp, _vp, _vp,
                              _vp * NCAT], C.c_int),

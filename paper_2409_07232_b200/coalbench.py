@@ -383,6 +383,12 @@ class CoalContext:
         self.handle = h
         self.device = device
 
+    def fast_kernel(self) -> str:
+        """Name of the FSBM_NUMERICS_FAST kernel this context dispatches to."""
+        k = C.c_int(0)
+        _lib.check(_lib.load().fsbm_ctx_fast_kernel(self.handle, C.byref(k)))
+        return {0: "unsupported", 1: "coal_fast", 2: "coal_dmma", 3: "coal_dmmag"}[k.value]
+
     def gain_table(self):
         """(lo, w_lo, w_hi, top), each [nkr*nkr] -- GainTable::at(i, j) at [i*nkr + j]."""
         n = self.nkr * self.nkr

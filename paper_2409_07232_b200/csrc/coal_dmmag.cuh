@@ -1,0 +1,741 @@
+// coal_dmmag.cuh -- FSBM_NUMERICS_FAST on the FP64 tensor cores (DMMA.8x8x4) for any bin
+// count whose flux targets stay within 9 bins of the owner (66 and 132 bins on the
+// equal-range grids of SURVEY 8(d); the tuned 32/33-bin kernel is coal_dmma.cuh).
+//
+// Same owner decomposition as coal_dmma.cuh / coal_fast.cuh (coalescence.cpp:204-339
+// reassociated): for a pair (a, b -> d) the row pass (owner o = i, stream s = j,
+// v = nb, f = na, loss -> a) and the column pass (o = j, s = i, v = na, f = nb,
+// loss -> b) compute per 8-row owner block and 8-point tile the GEMMs
+//     L[o,q]   = sum_s A(o,s) v_q[s]                 loss of bin o
+//     Z_t[o,q] = sum_s A(o,s) c_t(o,s) v_q[s]        gain into bin o+t, t = 0..TM-1
+// where c_t is the GainTable weight (coalescence.cpp:36-67) of cell (o,s) towards bin
+// o+t, restricted to the cells the owner owns (s < o; column pass and self-pair
+// diagonal s <= o, the latter halved, coalescence.cpp:293).  At 66/132 bins the
+// targets of a cell reach o+3 / o+5 (SURVEY 8(a) "band structure"), so unlike the
+// 33-bin kernel every offset has its own accumulator; the gain of row o+t lands in
+// the warp's own block or, past row 7, in a register "carry" block that is added to
+// the next block's rows at the Jacobi apply.
+//
+// K-step classes per (view, block): "far" steps (every cell targets {o, o+1} with
+// weights summing to 1) run two DMMAs -- X = sum A v and Y = sum A c0 v, with
+// Z_1 += X - Y --, "band" steps run the loss plus one DMMA per target offset present
+// in the tile, "upper" steps only the loss.  The weights are recomputed on the fly from
+// the mass grid (m = x_o + x_s, lo = o + delta(o - s), w = (x[lo+1] - m) / width) --
+// host-verified against the GainTable for every cell when the context is built --
+// so no pair-independent coefficient table occupies shared memory.
+//
+// Data movement: the per-pair kernel tables (K500, K750-K500) are pre-arranged on the
+// host in DMMA A-fragment order, chunked by K-steps ([pass][chunk][block][k][lane]),
+// and streamed into a 3-deep shared-memory ring by 1-D TMA bulk copies; the last warp
+// to release a buffer refills it.  The CTA's point spectra (all six categories) sit in
+// shared memory, point-minor and XOR-swizzled so B-fragment loads are conflict free.
+// A group whose 16 points share one pressure weight interpolates A in registers; a
+// group that straddles a level runs K500 against v and K750-K500 against w_q v.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "coal_dmma.cuh"
+
+namespace fsbm {
+
+constexpr int kGNST = 3;     // table-stage ring depth
+constexpr int kGNT = 2;      // 8-point N-tiles per warp (16 points per group)
+
+struct DmmagTables {
+    int nkr = 0, S = 0, KS = 0, nblk = 0, SR = 0, KCS = 0, NCH = 0, TM = 0, npairs = 0;
+    int item_base[kMaxPairs] = {};
+    size_t stage_elems = 0;      // double2 per stage = nblk * KCS * 32
+    double2 *stages = nullptr;   // [item][chunk][block][KCS][32]
+    double *consts = nullptr;    // x[SR+8] | invw[SR+8] (padded, finite)
+    int *cls = nullptr;          // [3 views][nblk] leading far K-steps kf
+    uint16_t *bmask = nullptr;   // [3 views][nblk][KS] gather target-offset masks
+    int *goff = nullptr;         // [3][nblk][KS] first gather fragment of the step
+    int *kg = nullptr;           // [3][nblk][2] K-step range holding gather entries
+    double *gcoef = nullptr;     // [entry][32] gather weight fragments
+};
+
+inline void free_dmmag_tables(DmmagTables &t) {
+    cudaFree(t.stages);
+    cudaFree(t.consts);
+    cudaFree(t.cls);
+    cudaFree(t.bmask);
+    cudaFree(t.goff);
+    cudaFree(t.kg);
+    cudaFree(t.gcoef);
+    t = DmmagTables{};
+}
+
+/// Builds the general DMMA tables; returns 0 with D.stages == nullptr when this grid is
+/// outside the kernel's envelope (the caller then uses coal_fast).
+inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::vector<int> &abd,
+                              const std::vector<double> &x, const double *t750, const double *t500,
+                              const std::vector<int32_t> &g_lo, const std::vector<double> &g_wlo,
+                              const std::vector<double> &g_whi, const std::vector<double> &g_top) {
+    D = DmmagTables{};
+    if (nkr < 8 || nkr > 136) return 0;
+    const int S = (nkr + 3) / 4 * 4, KS = S / 4, nblk = (nkr + 7) / 8, SR = nblk * 8;
+    // far-cell weights are recomputed on the fly: c0 = (x[o+1] - (x[o] + x[s])) / width[o]
+    // (one multiply by the reciprocal; checked against the GainTable per far cell below)
+    std::vector<double> xs(SR + 8), iw(SR + 8, 0.0);
+    for (int k = 0; k < SR + 8; ++k) xs[k] = x[std::min(k, nkr - 1)];
+    for (int k = 0; k + 1 < nkr; ++k) iw[k] = 1.0 / (x[k + 1] - x[k]);
+    int maxoff = 0; // furthest flux target above the owner max(i,j)
+    for (int o = 0; o < nkr; ++o)
+        for (int s = 0; s <= o; ++s) {
+            const size_t e = static_cast<size_t>(o) * nkr + s;
+            if (g_lo[e] < 0) maxoff = std::max(maxoff, nkr - 1 - o);
+            else {
+                if (g_lo[e] < o) return 0;
+                maxoff = std::max(maxoff, g_lo[e] - o + (g_whi[e] != 0.0 ? 1 : 0));
+            }
+        }
+    const int TM = maxoff < 2 ? 2 : maxoff < 4 ? 4 : maxoff < 6 ? 6 : maxoff < 10 ? 10 : 0;
+    if (TM == 0) return 0;
+    // ---- K-step classes per view (0 R-cross: s<o, 1 R-self: s<o + s==o halved, 2 C: s<=o) ----
+    // kf[V][b]: leading "far" K-steps of owner block b (every real cell s < o, targets
+    // {o, o+1}, weights summing to 1) -- their gains run through the X/Y identity.
+    // gm[V][b][ks]: target offsets t whose gather entry (owner rows 8b+r-t, cols 4ks..+3,
+    // far cells excluded) has a non-zero weight.
+    auto vmask = [&](int V, int o, int s) {
+        return V == 2 ? (s <= o ? 1.0 : 0.0) : (s < o ? 1.0 : (V == 1 && s == o ? 0.5 : 0.0));
+    };
+    std::vector<int> kfv(3 * nblk);
+    std::vector<uint16_t> bm(static_cast<size_t>(3) * nblk * KS, 0);
+    for (int V = 0; V < 3; ++V)
+        for (int b = 0; b < nblk; ++b) {
+            int kf = 0;
+            for (; kf < KS; ++kf) {
+                bool far = true;
+                for (int r = 0; r < 8 && far; ++r)
+                    for (int c = 0; c < 4 && far; ++c) {
+                        const int o = 8 * b + r, s = 4 * kf + c;
+                        if (o >= nkr || s >= nkr) continue; // A is zero there
+                        const size_t e = static_cast<size_t>(o) * nkr + s;
+                        const double c0 = (xs[o + 1] - (xs[o] + xs[s])) * iw[o];
+                        far = vmask(V, o, s) == 1.0 && s < o && g_lo[e] == o &&
+                              std::fabs(g_wlo[e] + g_whi[e] - 1.0) <= 4e-16 && std::fabs(c0 - g_wlo[e]) <= 4e-16;
+                    }
+                if (!far) break;
+            }
+            kfv[V * nblk + b] = kf;
+        }
+    // gather coefficient fragments (pair-independent): entry (V, b, ks, t) holds, per lane
+    // (row r = lane/4, col c = lane%4), the GainTable weight of cell (8b+r-t, 4ks+c)
+    // towards bin 8b+r, view-masked, zero for far cells (handled by the X/Y identity)
+    std::vector<int> goff(static_cast<size_t>(3) * nblk * KS, 0), kg(3 * nblk * 2, 0);
+    std::vector<double> gco;
+    for (int V = 0; V < 3; ++V)
+        for (int b = 0; b < nblk; ++b) {
+            int kgl = KS, kgh = 0;
+            for (int ks = 0; ks < KS; ++ks) {
+                double frag[16][32] = {};
+                uint16_t mask = 0;
+                for (int t = 0; t < TM; ++t)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int o = 8 * b + (lane >> 2) - t, s = 4 * ks + (lane & 3);
+                        if (o < 0 || o >= nkr || s >= nkr) continue;
+                        const double msk = vmask(V, o, s);
+                        if (msk == 0.0 || (s < o && ks < kfv[V * nblk + (o >> 3)])) continue;
+                        const size_t e = static_cast<size_t>(o) * nkr + s;
+                        double c = 0.0;
+                        if (g_lo[e] < 0) {
+                            if (t == nkr - 1 - o) c = g_top[e];
+                        } else {
+                            if (t == g_lo[e] - o) c += g_wlo[e];
+                            if (t == g_lo[e] - o + 1) c += g_whi[e];
+                        }
+                        c *= msk;
+                        frag[t][lane] = c;
+                        if (c != 0.0) mask |= 1u << t;
+                    }
+                bm[(static_cast<size_t>(V) * nblk + b) * KS + ks] = mask;
+                goff[(static_cast<size_t>(V) * nblk + b) * KS + ks] = static_cast<int>(gco.size() / 32);
+                for (int t = 0; t < TM; ++t)
+                    if (mask >> t & 1u) gco.insert(gco.end(), frag[t], frag[t] + 32);
+                if (mask) {
+                    kgl = std::min(kgl, ks);
+                    kgh = ks + 1;
+                }
+            }
+            kg[(V * nblk + b) * 2] = std::min(kgl, kgh);
+            kg[(V * nblk + b) * 2 + 1] = kgh;
+        }
+    if (gco.empty()) gco.assign(32, 0.0);
+    // ---- per-pass A fragments, K-chunked ----
+    const int KCS = nblk <= 9 ? 6 : 4;
+    const int NCH = (KS + KCS - 1) / KCS;
+    const size_t stage_elems = static_cast<size_t>(nblk) * KCS * 32;
+    int nitems = 0;
+    for (int p = 0; p < npairs; ++p) {
+        D.item_base[p] = nitems;
+        nitems += abd[3 * p] == abd[3 * p + 1] ? 1 : 2;
+    }
+    std::vector<double2> st(static_cast<size_t>(nitems) * NCH * stage_elems, double2{0.0, 0.0});
+    const size_t sq = static_cast<size_t>(nkr) * nkr;
+    for (int p = 0; p < npairs; ++p) {
+        const bool self = abd[3 * p] == abd[3 * p + 1];
+        const double *k750 = t750 + p * sq, *k500 = t500 + p * sq;
+        for (int X = 0; X < (self ? 1 : 2); ++X) {
+            double2 *base = st.data() + static_cast<size_t>(D.item_base[p] + X) * NCH * stage_elems;
+            for (int b = 0; b < nblk; ++b)
+                for (int ks = 0; ks < NCH * KCS; ++ks)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int o = 8 * b + (lane >> 2), s = 4 * ks + (lane & 3);
+                        if (o >= nkr || s >= nkr) continue;
+                        const int i = X == 0 ? o : s, j = X == 0 ? s : o; // reference cell (i,j)
+                        const size_t u = self ? static_cast<size_t>(std::min(i, j)) * nkr + std::max(i, j)
+                                              : static_cast<size_t>(i) * nkr + j;
+                        const int ch = ks / KCS, kl = ks % KCS;
+                        base[static_cast<size_t>(ch) * stage_elems + (static_cast<size_t>(b) * KCS + kl) * 32 + lane] =
+                            double2{k500[u], k750[u] - k500[u]};
+                    }
+        }
+    }
+    std::vector<double> consts(2 * (SR + 8));
+    std::copy(xs.begin(), xs.end(), consts.begin());
+    std::copy(iw.begin(), iw.end(), consts.begin() + SR + 8);
+    auto up = [](auto **dst, const auto &v) {
+        using T = typename std::remove_reference<decltype(v)>::type::value_type;
+        return cudaMalloc(reinterpret_cast<void **>(dst), sizeof(T) * v.size()) == cudaSuccess &&
+               cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    if (!up(&D.stages, st) || !up(&D.consts, consts) || !up(&D.cls, kfv) ||
+        !up(&D.bmask, bm) || !up(&D.goff, goff) || !up(&D.kg, kg) || !up(&D.gcoef, gco)) {
+        free_dmmag_tables(D);
+        fast_err() = "dmmag tables: device allocation failed";
+        return 6;
+    }
+    D.nkr = nkr;
+    D.S = S;
+    D.KS = KS;
+    D.nblk = nblk;
+    D.SR = SR;
+    D.KCS = KCS;
+    D.NCH = NCH;
+    D.TM = TM;
+    D.npairs = npairs;
+    D.stage_elems = stage_elems;
+    return 0;
+}
+
+struct DmmagArgs {
+    int KS, nblk, SR, KCS, NCH;
+    uint32_t nbatches, stage_elems;
+    int item_base[kMaxPairs];
+    const double2 *stages;
+    const double *consts;
+    const int *cls, *goff, *kg;
+    const uint16_t *bmask;
+    const double *gcoef;
+};
+
+typedef double DgAcc[kGNT][2];
+
+/// D[FC] -= L, D[PD] += H with compile-time categories.
+template <int FC, int PD>
+__device__ __forceinline__ void emitg_fp(double (&D)[kNCat][kGNT][2], const DgAcc &L, const DgAcc &H) {
+#pragma unroll
+    for (int nt = 0; nt < kGNT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            D[FC][nt][e] -= L[nt][e];
+            D[PD][nt][e] += H[nt][e];
+        }
+}
+
+__device__ __forceinline__ void emitg_switch(int sel, double (&D)[kNCat][kGNT][2], const DgAcc &L, const DgAcc &H) {
+#define FSBM_EMITG_CASE(F, P)                                                                      \
+    case F * kNCat + P: emitg_fp<F, P>(D, L, H); break;
+#define FSBM_EMITG_ROW(F)                                                                          \
+    FSBM_EMITG_CASE(F, 0) FSBM_EMITG_CASE(F, 1) FSBM_EMITG_CASE(F, 2) FSBM_EMITG_CASE(F, 3)        \
+    FSBM_EMITG_CASE(F, 4) FSBM_EMITG_CASE(F, 5)
+    switch (sel) {
+        FSBM_EMITG_ROW(0)
+        FSBM_EMITG_ROW(1)
+        FSBM_EMITG_ROW(2)
+        FSBM_EMITG_ROW(3)
+        FSBM_EMITG_ROW(4)
+        FSBM_EMITG_ROW(5)
+    default: break;
+    }
+#undef FSBM_EMITG_ROW
+#undef FSBM_EMITG_CASE
+}
+
+/// Position in the CTA's stage sequence: pass (pair p, X = 0 row / 1 column), K-chunk ch.
+struct GStage {
+    int p, X, ch;
+};
+
+template <int TM, int G, int MAXW>
+__global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, DmmagArgs F) {
+    constexpr int NT = kGNT, NP = G * 16, NST = kGNST;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nkr = A.nkr, SR = F.SR, KS = F.KS, KCS = F.KCS, NCH = F.NCH, NB = F.nblk;
+    const uint32_t SE = F.stage_elems;
+    double2 *stg = reinterpret_cast<double2 *>(smem_raw);                          // [NST][SE]
+    double *work = reinterpret_cast<double *>(stg + NST * static_cast<size_t>(SE)); // [6][SR][NP]
+    double *carry = work + static_cast<size_t>(kNCat) * SR * NP;                  // [6][NB][NP]
+    double *xs = carry + static_cast<size_t>(kNCat) * NB * NP;                     // [SR+8]
+    double *iw = xs + SR + 8;                                                       // [SR+8]
+    double *wts = iw + SR + 8;                                                      // [NP]
+    unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP);     // [NP]
+    unsigned long long *ptrip = act + NP;                                           // [NP]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);                      // [NST]
+    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + NST);                      // [NP]
+    int *pfail = reinterpret_cast<int *>(pidx + NP);                                // [NP]
+    int *kfs = pfail + NP;                                                          // [3][NB]
+    int *kgs = kfs + 3 * NB;                                                        // [3][NB][2]
+    int *gofs = kgs + 6 * NB;                                                       // [3][NB][KS]
+    uint16_t *bms = reinterpret_cast<uint16_t *>(gofs + 3 * NB * KS);               // [3][NB][KS]
+    __shared__ unsigned long long cta_act;
+    __shared__ int kzg[G][kNCat];
+    __shared__ int kzc[kNCat];
+    __shared__ int relcnt[NST];
+
+    const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
+    const int wid = tid >> 5, lane = tid & 31;
+    const int g = wid / NB, b = wid % NB;
+    const int lr = lane >> 2, lc = lane & 3;
+    const int o = 8 * b + lr;
+    const int qg = g * 16;
+    if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
+    const uint32_t nact = *A.nactive;
+    const int npairs = A.pairs.npairs;
+    const unsigned long long full_evals = static_cast<unsigned long long>(npairs) * nkr * nkr;
+    const int self_tri = nkr * (nkr + 1) / 2, cross_sq = nkr * nkr;
+    const double dt = A.dt_sub;
+    const uint32_t sbytes = SE * static_cast<uint32_t>(sizeof(double2));
+    unsigned long long tr_acc = 0, pt_acc = 0, ev_acc = 0;
+
+    // point-minor spectra, bit 3 of the point index swizzled by the bin's parity: the
+    // four K rows of a B fragment (8 points each) then hit disjoint bank halves
+    auto W = [&](int c, int s, int q) -> double & {
+        return work[(static_cast<size_t>(c) * SR + s) * NP + (q ^ ((s & 1) << 3))];
+    };
+
+    for (int f = tid; f < 2 * (SR + 8); f += nthr) xs[f] = F.consts[f];
+    for (int f = tid; f < 3 * NB; f += nthr) kfs[f] = F.cls[f];
+    for (int f = tid; f < 6 * NB; f += nthr) kgs[f] = F.kg[f];
+    for (int f = tid; f < 3 * NB * KS; f += nthr) {
+        gofs[f] = F.goff[f];
+        bms[f] = F.bmask[f];
+    }
+    for (int f = tid; f < kNCat * SR * NP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) mbar_init(&mbar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const double xo = xs[o], xo1 = xs[o + 1], iwo = iw[o];
+    uint32_t pbase = 0;
+
+    for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
+         batch += gridDim.x) {
+        for (int q = tid; q < NP; q += nthr) {
+            const uint32_t idx = batch * static_cast<uint32_t>(NP) + q;
+            const bool live = idx < nact;
+            const uint32_t p = live ? A.active[idx] : 0xffffffffu;
+            pidx[q] = p;
+            wts[q] = live ? pressure_weight(A.pressure[p]) : 0.0;
+            pfail[q] = live ? 0 : 1;
+            ptrip[q] = 0;
+        }
+        __syncthreads();
+        { // spectra -> work: a warp instruction covers 4 points x 8 consecutive bins
+            const int NQ = kNCat * NP / 4;
+            const int qs = lane >> 3, kc = lane & 7;
+            for (int u = wid; u < NQ; u += NW) {
+                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+                const uint32_t p = pidx[q];
+                const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
+#pragma unroll 4
+                for (int k = kc; k < nkr; k += 8) W(c, k, q) = p != 0xffffffffu ? __ldg(src + k) : 0.0;
+            }
+        }
+        __syncthreads();
+
+        for (int sub = 0; sub < A.substeps; ++sub) {
+            if (tid == 0) cta_act = 0ull;
+            if (tid < G * kNCat) kzg[tid / kNCat][tid % kNCat] = -1;
+            if (tid < kNCat) kzc[tid] = -1;
+            if (tid < NST) relcnt[tid] = 0;
+            for (int f = tid; f < kNCat * NB * NP; f += nthr) carry[f] = 0.0;
+            __syncthreads();
+            for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
+                unsigned nz = 0;
+                for (int c = 0; c < kNCat; ++c) { // scanned from the top: last non-zero bin
+                    int l = nkr - 1;
+                    while (l >= 0 && W(c, l, q) == 0.0) --l;
+                    nz |= l >= 0 ? (1u << c) : 0u;
+                    if (l >= 0 && pfail[q] == 0) {
+                        atomicMax(&kzg[q / 16][c], l);
+                        atomicMax(&kzc[c], l);
+                    }
+                }
+                unsigned long long m = 0, trip = 0;
+                for (int pp = 0; pp < npairs; ++pp)
+                    if (nz >> A.pairs.a[pp] & 1u) {
+                        m |= 1ull << pp;
+                        trip += A.pairs.a[pp] == A.pairs.b[pp] ? self_tri : cross_sq;
+                    }
+                if (pfail[q] == 0) {
+                    act[q] = m;
+                    atomicOr(&cta_act, m);
+                    ptrip[q] += trip;
+                } else {
+                    act[q] = 0;
+                }
+            }
+            __syncthreads();
+            const unsigned long long amask = cta_act;
+
+            // ---- the CTA's stage sequence (identical in every warp) ----
+            auto pass_nch = [&](int p, int X) -> int {
+                const int pa = A.pairs.a[p], pb = A.pairs.b[p];
+                const int fc = X == 0 ? pa : pb, sc = X == 0 ? pb : pa;
+                if (kzc[fc] < 0 || kzc[sc] < 0) return 0; // every product of the pass is zero
+                return min(NCH, kzc[sc] / (4 * KCS) + 1);
+            };
+            auto advance = [&](GStage s) -> GStage { // next stage strictly after s
+                if (s.p < 0) return s;
+                if (s.ch + 1 < pass_nch(s.p, s.X)) return GStage{s.p, s.X, s.ch + 1};
+                int p = s.p, X = s.X;
+                while (true) {
+                    ++X;
+                    if (X > (A.pairs.a[p] == A.pairs.b[p] ? 0 : 1)) {
+                        const unsigned long long rest = amask & ~((2ull << p) - 1ull);
+                        if (!rest) return GStage{-1, 0, 0};
+                        p = __ffsll(static_cast<long long>(rest)) - 1;
+                        X = 0;
+                    }
+                    if (pass_nch(p, X) > 0) return GStage{p, X, 0};
+                }
+            };
+            auto issue = [&](GStage s, int buf) {
+                mbar_expect_tx(&mbar[buf], sbytes);
+                const size_t off = (static_cast<size_t>(F.item_base[s.p] + s.X) * NCH + s.ch) * SE;
+                tma_bulk_g2s(stg + static_cast<size_t>(buf) * SE, F.stages + off, sbytes, &mbar[buf]);
+            };
+            GStage cur{-1, 0, 0};
+            if (amask) {
+                const int p0 = __ffsll(static_cast<long long>(amask)) - 1;
+                cur = pass_nch(p0, 0) > 0 ? GStage{p0, 0, 0} : advance(GStage{p0, 0, NCH});
+            }
+            if (tid == 0) { // prime the ring
+                fence_proxy_async();
+                GStage s = cur;
+                for (int i = 0; i < NST && s.p >= 0; ++i, s = advance(s)) issue(s, (pbase + i) % NST);
+            }
+            __syncthreads();
+
+            double D[kNCat][NT][2];
+#pragma unroll
+            for (int c = 0; c < kNCat; ++c)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) D[c][nt][0] = D[c][nt][1] = 0.0;
+            // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
+            // Z[t]: gain of owner rows o-t into this warp's rows o (gather form, far cells excluded)
+            double L[NT][2], Xf[NT][2], Yf[NT][2], Z[TM][NT][2];
+            int fcat = 0, scat = 0, pd = 0, V = 0, kf = 0, kzs = -1, nchp = 0;
+            bool skip = true, uni = true;
+            double wu = 0.0, wq[NT] = {0.0, 0.0};
+            bool on[NT][2];
+            int n = 0;
+            while (cur.p >= 0) {
+                const uint32_t m = pbase + n;
+                const int buf = m % NST;
+                if (cur.ch == 0) {
+                    const int pa = A.pairs.a[cur.p], pb = A.pairs.b[cur.p];
+                    const bool self = pa == pb;
+                    fcat = cur.X == 0 ? pa : pb;
+                    scat = cur.X == 0 ? pb : pa;
+                    pd = A.pairs.d[cur.p];
+                    V = cur.X == 1 ? 2 : (self ? 1 : 0);
+                    kf = kfs[V * NB + b];
+                    kzs = kzg[g][scat];
+                    nchp = pass_nch(cur.p, cur.X);
+                    // every owner row this warp reads (8b-TM+1 .. 8b+7) or the stream is zero
+                    skip = !(8 * b - (TM - 1) <= kzg[g][fcat] && kzs >= 0);
+                    wu = wts[qg];
+                    bool allu = true;
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        wq[nt] = wts[qg + 8 * nt + lr];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int q = qg + 8 * nt + 2 * lc + e;
+                            on[nt][e] = act[q] >> cur.p & 1ull;
+                            allu = allu && wts[q] == wu;
+                        }
+                    }
+                    uni = __all_sync(0xffffffffu, allu);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            L[nt][e] = Xf[nt][e] = Yf[nt][e] = 0.0;
+#pragma unroll
+                            for (int t = 0; t < TM; ++t) Z[t][nt][e] = 0.0;
+                        }
+                }
+                mbar_wait(&mbar[buf], (m / NST) & 1u);
+                if (!skip) {
+                    const double2 *sb = stg + static_cast<size_t>(buf) * SE;
+                    const double2 *sa = sb + static_cast<size_t>(b) * KCS * 32 + lane;
+                    const int k0 = cur.ch * KCS;
+                    const int kend = min(KS, min(k0 + KCS, (kzs >> 2) + 1));
+                    const int vb = V * NB + b;
+                    const int kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
+                    // B fragments (and w-scaled copies for a straddling group)
+                    auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            bv[nt] = W(scat, 4 * ks + lc, qg + 8 * nt + lr);
+                            bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
+                        }
+                    };
+                    auto far_step = [&](int ks, double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
+                        const double c0 = (xo1 - (xo + xs[4 * ks + lc])) * iwo;
+                        const double a2 = a * c0, ad2 = ad * c0;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            dmma(Xf[nt][0], Xf[nt][1], a, bv[nt]);
+                            dmma(Yf[nt][0], Yf[nt][1], a2, bv[nt]);
+                            if (!uni) {
+                                dmma(Xf[nt][0], Xf[nt][1], ad, bw[nt]);
+                                dmma(Yf[nt][0], Yf[nt][1], ad2, bw[nt]);
+                            }
+                        }
+                    };
+                    auto loss_step = [&](double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            dmma(L[nt][0], L[nt][1], a, bv[nt]);
+                            if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
+                        }
+                    };
+                    int ks = k0;
+                    // (1) far steps before any gather entry
+#pragma unroll 2
+                    for (; ks < min(kend, min(kf, kgl)); ++ks) {
+                        const double2 kk = sa[(ks - k0) * 32];
+                        double bv[NT], bw[NT];
+                        loadb(ks, bv, bw);
+                        far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                    }
+                    // (2) general steps: far or loss, plus the gather entries of the step
+                    for (; ks < min(kend, max(kf, kgh)); ++ks) {
+                        const double2 kk = sa[(ks - k0) * 32];
+                        double bv[NT], bw[NT];
+                        loadb(ks, bv, bw);
+                        const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
+                        if (ks < kf) far_step(ks, a, ad, bv, bw);
+                        else loss_step(a, ad, bv, bw);
+                        const unsigned gmk = bms[vb * KS + ks];
+                        if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
+                            const double *gc = F.gcoef + static_cast<size_t>(gofs[vb * KS + ks]) * 32 + lane;
+                            int rk = 0;
+#pragma unroll
+                            for (int t = 0; t < TM; ++t) {
+                                if (gmk >> t & 1u) {
+                                    const double c = __ldg(gc + 32 * rk);
+                                    ++rk;
+                                    double at = a, adt = ad;
+                                    if (t > 0) {
+                                        const int ot = max(o - t, 0); // rows < 0 carry c == 0
+                                        const double2 k2 = sb[static_cast<size_t>(ot >> 3) * KCS * 32 + (ks - k0) * 32 +
+                                                              (((ot & 7) << 2) | lc)];
+                                        at = uni ? fma(wu, k2.y, k2.x) : k2.x;
+                                        adt = k2.y;
+                                    }
+                                    const double a2 = at * c, ad2 = adt * c;
+#pragma unroll
+                                    for (int nt = 0; nt < NT; ++nt) {
+                                        dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
+                                        if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    // (3) loss-only steps above the band
+#pragma unroll 2
+                    for (; ks < kend; ++ks) {
+                        const double2 kk = sa[(ks - k0) * 32];
+                        double bv[NT], bw[NT];
+                        loadb(ks, bv, bw);
+                        loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                    }
+                    if (cur.ch == nchp - 1) { // pass complete: emission
+                        DgAcc Lv, Hv;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int q = qg + 8 * nt + 2 * lc + e;
+                                const double f = on[nt][e] ? W(fcat, o, q) : 0.0; // dt: at the apply
+                                Lv[nt][e] = f * (L[nt][e] + Xf[nt][e]);
+                                const double hi = f * (Xf[nt][e] - Yf[nt][e]); // far cells -> row o+1
+                                const double up = __shfl_up_sync(0xffffffffu, hi, 4);
+                                double h = f * (Yf[nt][e] + Z[0][nt][e]);
+                                if (lr > 0) h += up;
+                                if (lr == 7) carry[(static_cast<size_t>(pd) * NB + b) * NP + q] += hi;
+#pragma unroll
+                                for (int t = 1; t < TM; ++t) {
+                                    const int ot = o - t;
+                                    const double ft = on[nt][e] && ot >= 0 ? W(fcat, ot, q) : 0.0;
+                                    h = fma(ft, Z[t][nt][e], h);
+                                }
+                                Hv[nt][e] = h;
+                            }
+                        emitg_switch(fcat * kNCat + pd, D, Lv, Hv);
+                    }
+                }
+                // release buffer `buf`; the last warp out refills it NST stages ahead
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    const int old = atomicAdd(&relcnt[buf], 1);
+                    if (old == NW - 1) {
+                        relcnt[buf] = 0;
+                        __threadfence_block();
+                        GStage s2 = cur;
+                        for (int i = 0; i < NST; ++i) s2 = advance(s2);
+                        if (s2.p >= 0) {
+                            fence_proxy_async();
+                            issue(s2, buf);
+                        }
+                    }
+                }
+                cur = advance(cur);
+                ++n;
+            }
+            pbase += n;
+            // ---- Jacobi apply (coalescence.cpp:313-328): own rows, then the block-head carries ----
+            __syncthreads();
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int q = qg + 8 * nt + 2 * lc + e;
+#pragma unroll
+                    for (int c = 0; c < kNCat; ++c) W(c, o, q) = fma(dt, D[c][nt][e], W(c, o, q));
+                }
+            __syncthreads();
+            for (int f = tid; f < kNCat * (NB - 1) * NP; f += nthr) {
+                const int q = f % NP, cb = f / NP, c = cb / (NB - 1), bb = cb % (NB - 1);
+                const int row = 8 * (bb + 1);
+                W(c, row, q) = fma(dt, carry[(static_cast<size_t>(c) * NB + bb) * NP + q], W(c, row, q));
+            }
+            __syncthreads();
+            for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
+                for (int k = wid; k < nkr; k += NW)
+                    for (int q = lane; q < NP; q += 32) {
+                        const uint32_t p = pidx[q];
+                        if (p == 0xffffffffu || pfail[q] != 0) continue;
+                        if (W(c, k, q) < 0.0) {
+                            report_stiffness(A, p, c, k);
+                            pfail[q] = 2;
+                        }
+                    }
+            __syncthreads();
+            for (int q = tid; q < NP; q += nthr)
+                if (pfail[q] == 2) pfail[q] = 3;
+        }
+        { // write back, coalesced like the load
+            const int NQ = kNCat * NP / 4;
+            const int qs = lane >> 3, kc = lane & 7;
+            for (int u = wid; u < NQ; u += NW) {
+                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+                const uint32_t p = pidx[q];
+                if (p == 0xffffffffu) continue;
+                double *dst = A.bins[c] + static_cast<size_t>(p) * nkr;
+#pragma unroll 4
+                for (int k = kc; k < nkr; k += 8) dst[k] = W(c, k, q);
+            }
+        }
+        for (int q = tid; q < NP; q += nthr) {
+            if (pidx[q] == 0xffffffffu || pfail[q] != 0) continue;
+            tr_acc += ptrip[q];
+            pt_acc += 1;
+            ev_acc += A.kernel_strategy ? ptrip[q] : full_evals;
+        }
+        __syncthreads();
+    }
+    for (int of = 16; of > 0; of >>= 1) {
+        tr_acc += __shfl_down_sync(0xffffffffu, tr_acc, of);
+        pt_acc += __shfl_down_sync(0xffffffffu, pt_acc, of);
+        ev_acc += __shfl_down_sync(0xffffffffu, ev_acc, of);
+    }
+    if (lane == 0 && (tr_acc | pt_acc | ev_acc)) {
+        atomicAdd(&A.counters[0], tr_acc);
+        atomicAdd(&A.counters[1], pt_acc);
+        atomicAdd(&A.counters[2], ev_acc);
+    }
+}
+
+inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP) {
+    return static_cast<size_t>(kGNST) * T.stage_elems * sizeof(double2) +
+           (static_cast<size_t>(kNCat) * T.SR * NP + static_cast<size_t>(kNCat) * T.nblk * NP + 2 * (T.SR + 8) + NP) *
+               sizeof(double) +
+           NP * 16 + kGNST * 8 + NP * 8 + 9 * T.nblk * 4 + 3 * T.nblk * T.KS * 6 + 16;
+}
+
+template <int TM, int G, int MAXW>
+inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
+    constexpr int NP = G * 16;
+    if (T.nblk * G > MAXW) return -1;
+    const size_t smem = dmmag_smem_bytes(T, NP);
+    if (smem > 227 * 1024) return -1;
+    DmmagArgs F{};
+    F.KS = T.KS;
+    F.nblk = T.nblk;
+    F.SR = T.SR;
+    F.KCS = T.KCS;
+    F.NCH = T.NCH;
+    F.nbatches = (A.nactive_host + NP - 1) / NP;
+    F.stage_elems = static_cast<uint32_t>(T.stage_elems);
+    for (int p = 0; p < kMaxPairs; ++p) F.item_base[p] = T.item_base[p];
+    F.stages = T.stages;
+    F.consts = T.consts;
+    F.cls = T.cls;
+    F.bmask = T.bmask;
+    F.goff = T.goff;
+    F.kg = T.kg;
+    F.gcoef = T.gcoef;
+    auto kern = coal_dmmag_kernel<TM, G, MAXW>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess) {
+        fast_err() = "dmmag path: cannot reserve shared memory";
+        return 6;
+    }
+    const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
+    kern<<<grid, T.nblk * G * 32, smem, s>>>(A, F);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fast_err() = std::string("dmmag path launch: ") + cudaGetErrorString(e);
+        return 6;
+    }
+    return 0;
+}
+
+/// Returns -1 when this geometry cannot run the general DMMA path.  One CTA of nblk
+/// warps (<= 12 so the register file allows 168 per thread) per 16-point batch.
+inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
+    if (!T.stages || A.nkr != T.nkr || T.nblk > 12) return -1;
+    switch (T.TM) {
+    case 2: return launch_dmmag_t<2, 1, 12>(T, A, num_sms, s);
+    case 4: return launch_dmmag_t<4, 1, 12>(T, A, num_sms, s);
+    case 6: return launch_dmmag_t<6, 1, 12>(T, A, num_sms, s);
+    case 10: return launch_dmmag_t<10, 1, 12>(T, A, num_sms, s);
+    default: return -1;
+    }
+}
+
+} // namespace fsbm

@@ -24,6 +24,7 @@
 #include "coal_exact.cuh"
 #include "coal_fast.cuh"
 #include "coal_dmma.cuh"
+#include "coal_dmmag.cuh"
 #include "fsbm_common.cuh"
 
 using namespace fsbm;
@@ -80,7 +81,8 @@ struct fsbm_ctx {
     double *d_gwlo = nullptr, *d_gwhi = nullptr, *d_gtop = nullptr;
     FastTables fast{};
     DmmaTables dmma{};
-    int fast_kernel = 0; // 0 auto, 1 direct (coal_fast), 2 dmma (FSBM_FAST_KERNEL)
+    DmmagTables dmmag{};
+    int fast_kernel = 0; // 0 auto, 1 direct (coal_fast), 2 dmma, 3 dmmag (FSBM_FAST_KERNEL)
     // per-step workspace (grown on demand, never per-step allocated in steady state):
     // one compaction workspace per pipeline slot (the host path runs 3 chunks in flight)
     static constexpr int kSlots = 3;
@@ -155,6 +157,7 @@ void free_ctx(fsbm_ctx *c) {
     cudaFree(c->d_gtop);
     free_fast_tables(c->fast);
     free_dmma_tables(c->dmma);
+    free_dmmag_tables(c->dmmag);
     for (int k = 0; k < fsbm_ctx::kSlots; ++k) {
         cudaFree(c->d_ws[k]);
         cudaFree(c->d_chunk[k]);
@@ -384,10 +387,13 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
         FSBM_CUDA_TRY(cudaGetLastError());
     } else {
         int st = -1;
-        if (c->fast_kernel != 1) st = launch_dmma(c->dmma, c->fast, A, c->num_sms, s);
+        if (c->fast_kernel == 0 || c->fast_kernel == 2) st = launch_dmma(c->dmma, c->fast, A, c->num_sms, s);
+        if (st > 0) return fail(st, fast_last_error());
+        if (st < 0 && (c->fast_kernel == 0 || c->fast_kernel == 3)) st = launch_dmmag(c->dmmag, A, c->num_sms, s);
         if (st > 0) return fail(st, fast_last_error());
         if (st < 0) {
             if (c->fast_kernel == 2) return fail(FSBM_CONFIG, "FSBM_FAST_KERNEL=dmma unsupported for this nkr");
+            if (c->fast_kernel == 3) return fail(FSBM_CONFIG, "FSBM_FAST_KERNEL=dmmag unsupported for this nkr");
             if (int st2 = launch_fast(c->fast, A, c->num_sms, s)) return fail(st2, fast_last_error());
         }
     }
@@ -613,9 +619,13 @@ int fsbm_ctx_create(int device, int nkr, const double *x, double ratio, int npai
                                c->g_whi, c->g_top);
         if (!st) st = build_dmma_tables(c->dmma, nkr, npairs, c->abd, t750, t500, c->g_lo,
                                         c->g_wlo, c->g_whi, c->g_top);
+        if (!st) st = build_dmmag_tables(c->dmmag, nkr, npairs, c->abd, c->x, t750, t500, c->g_lo,
+                                         c->g_wlo, c->g_whi, c->g_top);
         if (st) fail(st, fast_last_error());
-        if (const char *ev = std::getenv("FSBM_FAST_KERNEL"))
-            c->fast_kernel = std::string(ev) == "direct" ? 1 : std::string(ev) == "dmma" ? 2 : 0;
+        if (const char *ev = std::getenv("FSBM_FAST_KERNEL")) {
+            const std::string k(ev);
+            c->fast_kernel = k == "direct" ? 1 : k == "dmma" ? 2 : k == "dmmag" ? 3 : 0;
+        }
     }
     if (st) {
         free_ctx(c);
@@ -909,6 +919,19 @@ int fsbm_probe_fp64_peak(int device, double *tflops) {
     if (err != cudaSuccess) return fail(FSBM_CUDA, cudaGetErrorString(err));
     const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * 256;
     *tflops = flops / (ms * 1e-3) / 1e12;
+    return FSBM_OK;
+}
+
+int fsbm_ctx_fast_kernel(const fsbm_ctx *c, int *kernel) {
+    if (!c || !kernel) return fail(FSBM_DOMAIN, "null context");
+    const bool dm = c->dmma.blob && c->dmma.nkr == c->nkr;
+    const bool dg = c->dmmag.stages && c->dmmag.nkr == c->nkr && c->dmmag.nblk <= 12;
+    switch (c->fast_kernel) {
+    case 1: *kernel = 1; break;
+    case 2: *kernel = dm ? 2 : 0; break;
+    case 3: *kernel = dg ? 3 : 0; break;
+    default: *kernel = dm ? 2 : dg ? 3 : 1; break;
+    }
     return FSBM_OK;
 }
 
