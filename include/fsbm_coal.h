@@ -167,7 +167,7 @@ int fsbm_ctx_last_timing(const fsbm_ctx *ctx, float *coal_kernel_ms, int *launch
 
 /* Which FSBM_NUMERICS_FAST kernel this context dispatches to: 1 coal_fast (direct
  * FP64, any nkr), 2 coal_dmma (FP64 tensor cores, nkr 32/33), 3 coal_dmmag (FP64
- * tensor cores, general band grids up to 96 bins).  FSBM_FAST_KERNEL=direct|dmma|dmmag
+ * tensor cores, general band grids up to ~190 bins).  FSBM_FAST_KERNEL=direct|dmma|dmmag
  * in the environment at fsbm_ctx_create forces one (A/B and parity testing). */
 int fsbm_ctx_fast_kernel(const fsbm_ctx *ctx, int *kernel);
 

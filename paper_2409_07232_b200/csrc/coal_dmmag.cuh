@@ -77,7 +77,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                               const std::vector<int32_t> &g_lo, const std::vector<double> &g_wlo,
                               const std::vector<double> &g_whi, const std::vector<double> &g_top) {
     D = DmmagTables{};
-    if (nkr < 8 || nkr > 136) return 0;
+    if (nkr < 8 || nkr > 192) return 0;
     const int S = (nkr + 3) / 4 * 4, KS = S / 4, nblk = (nkr + 7) / 8, SR = nblk * 8;
     // far-cell weights are recomputed on the fly: c0 = (x[o+1] - (x[o] + x[s])) / width[o]
     // (one multiply by the reciprocal; checked against the GainTable per far cell below)
@@ -167,7 +167,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
         }
     if (gco.empty()) gco.assign(32, 0.0);
     // ---- per-pass A fragments, K-chunked ----
-    const int KCS = nblk <= 9 ? 6 : 4;
+    const int KCS = nblk <= 9 ? 6 : nblk <= 12 ? 4 : 3;
     const int NCH = (KS + KCS - 1) / KCS;
     const size_t stage_elems = static_cast<size_t>(nblk) * KCS * 32;
     int nitems = 0;
@@ -236,35 +236,27 @@ struct DmmagArgs {
 
 typedef double DgAcc[kGNT][2];
 
-/// D[FC] -= L, D[PD] += H with compile-time categories.
-template <int FC, int PD>
-__device__ __forceinline__ void emitg_fp(double (&D)[kNCat][kGNT][2], const DgAcc &L, const DgAcc &H) {
+// ---- TMEM as the delta store (tcgen05.ld/st, 32x32b shape: thread i <-> TMEM lane base+i) ----
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, double (&v)[4]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int nt = 0; nt < kGNT; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            D[FC][nt][e] -= L[nt][e];
-            D[PD][nt][e] += H[nt][e];
-        }
+    for (int i = 0; i < 4; ++i) v[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
 }
-
-__device__ __forceinline__ void emitg_switch(int sel, double (&D)[kNCat][kGNT][2], const DgAcc &L, const DgAcc &H) {
-#define FSBM_EMITG_CASE(F, P)                                                                      \
-    case F * kNCat + P: emitg_fp<F, P>(D, L, H); break;
-#define FSBM_EMITG_ROW(F)                                                                          \
-    FSBM_EMITG_CASE(F, 0) FSBM_EMITG_CASE(F, 1) FSBM_EMITG_CASE(F, 2) FSBM_EMITG_CASE(F, 3)        \
-    FSBM_EMITG_CASE(F, 4) FSBM_EMITG_CASE(F, 5)
-    switch (sel) {
-        FSBM_EMITG_ROW(0)
-        FSBM_EMITG_ROW(1)
-        FSBM_EMITG_ROW(2)
-        FSBM_EMITG_ROW(3)
-        FSBM_EMITG_ROW(4)
-        FSBM_EMITG_ROW(5)
-    default: break;
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const double (&v)[4]) {
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r[2 * i] = static_cast<uint32_t>(__double2loint(v[i]));
+        r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v[i]));
     }
-#undef FSBM_EMITG_ROW
-#undef FSBM_EMITG_CASE
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 /// Position in the CTA's stage sequence: pass (pair p, X = 0 row / 1 column), K-chunk ch.
@@ -272,11 +264,14 @@ struct GStage {
     int p, X, ch;
 };
 
+constexpr int kGTmemCols = 96; // per warp: 2 blocks x 6 categories x 4 doubles (2 columns each)
+
 template <int TM, int G, int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, DmmagArgs F) {
     constexpr int NT = kGNT, NP = G * 16, NST = kGNST;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nkr = A.nkr, SR = F.SR, KS = F.KS, KCS = F.KCS, NCH = F.NCH, NB = F.nblk;
+    const int NWP = (NB + 1) / 2; // warps per point group: one balanced block pair each
     const uint32_t SE = F.stage_elems;
     double2 *stg = reinterpret_cast<double2 *>(smem_raw);                          // [NST][SE]
     double *work = reinterpret_cast<double *>(stg + NST * static_cast<size_t>(SE)); // [6][SR][NP]
@@ -297,12 +292,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     __shared__ int kzg[G][kNCat];
     __shared__ int kzc[kNCat];
     __shared__ int relcnt[NST];
+    __shared__ uint32_t tmem_base;
+    __shared__ unsigned long long cnt_sh[3];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
     const int wid = tid >> 5, lane = tid & 31;
-    const int g = wid / NB, b = wid % NB;
+    const int g = wid / NWP, pw = wid % NWP;
+    const int nbw = pw == NB - 1 - pw ? 1 : 2;          // blocks owned by this warp
     const int lr = lane >> 2, lc = lane & 3;
-    const int o = 8 * b + lr;
     const int qg = g * 16;
     if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const uint32_t nact = *A.nactive;
@@ -311,7 +308,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     const int self_tri = nkr * (nkr + 1) / 2, cross_sq = nkr * nkr;
     const double dt = A.dt_sub;
     const uint32_t sbytes = SE * static_cast<uint32_t>(sizeof(double2));
-    unsigned long long tr_acc = 0, pt_acc = 0, ev_acc = 0;
 
     // point-minor spectra, bit 3 of the point index swizzled by the bin's parity: the
     // four K rows of a B fragment (8 points each) then hit disjoint bank halves
@@ -327,12 +323,20 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
         bms[f] = F.bmask[f];
     }
     for (int f = tid; f < kNCat * SR * NP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
+    if (tid < 3) cnt_sh[tid] = 0ull;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) mbar_init(&mbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (wid == 0) { // the whole TMEM of the SM: deltas of every warp's blocks
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    const double xo = xs[o], xo1 = xs[o + 1], iwo = iw[o];
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this warp's delta columns: lanes 32*(wid%4).., columns (wid/4)*96 + j*48 + c*8
+    const uint32_t tmw = tmem_base + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + (wid >> 2) * kGTmemCols;
     uint32_t pbase = 0;
 
     for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
@@ -366,6 +370,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
             if (tid < kNCat) kzc[tid] = -1;
             if (tid < NST) relcnt[tid] = 0;
             for (int f = tid; f < kNCat * NB * NP; f += nthr) carry[f] = 0.0;
+            {
+                const double z[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int k = 0; k < 2 * kNCat; ++k) tm_st4(tmw + 8 * k, z);
+            }
             __syncthreads();
             for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
                 unsigned nz = 0;
@@ -434,16 +442,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
             }
             __syncthreads();
 
-            double D[kNCat][NT][2];
-#pragma unroll
-            for (int c = 0; c < kNCat; ++c)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) D[c][nt][0] = D[c][nt][1] = 0.0;
-            // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
-            // Z[t]: gain of owner rows o-t into this warp's rows o (gather form, far cells excluded)
-            double L[NT][2], Xf[NT][2], Yf[NT][2], Z[TM][NT][2];
-            int fcat = 0, scat = 0, pd = 0, V = 0, kf = 0, kzs = -1, nchp = 0;
-            bool skip = true, uni = true;
+            int fcat = 0, scat = 0, pd = 0, V = 0, kzs = -1;
+            bool uni = true;
             double wu = 0.0, wq[NT] = {0.0, 0.0};
             bool on[NT][2];
             int n = 0;
@@ -452,16 +452,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 const int buf = m % NST;
                 if (cur.ch == 0) {
                     const int pa = A.pairs.a[cur.p], pb = A.pairs.b[cur.p];
-                    const bool self = pa == pb;
                     fcat = cur.X == 0 ? pa : pb;
                     scat = cur.X == 0 ? pb : pa;
                     pd = A.pairs.d[cur.p];
-                    V = cur.X == 1 ? 2 : (self ? 1 : 0);
-                    kf = kfs[V * NB + b];
+                    V = cur.X == 1 ? 2 : (pa == pb ? 1 : 0);
                     kzs = kzg[g][scat];
-                    nchp = pass_nch(cur.p, cur.X);
-                    // every owner row this warp reads (8b-TM+1 .. 8b+7) or the stream is zero
-                    skip = !(8 * b - (TM - 1) <= kzg[g][fcat] && kzs >= 0);
                     wu = wts[qg];
                     bool allu = true;
 #pragma unroll
@@ -475,6 +470,23 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         }
                     }
                     uni = __all_sync(0xffffffffu, allu);
+                }
+                mbar_wait(&mbar[buf], (m / NST) & 1u);
+                const double2 *sb = stg + static_cast<size_t>(buf) * SE;
+                const int k0 = cur.ch * KCS;
+                const int kend = min(KS, min(k0 + KCS, (kzs >> 2) + 1));
+                for (int j = 0; j < nbw; ++j) {
+                    const int b = j == 0 ? pw : NB - 1 - pw;
+                    const int o = 8 * b + lr;
+                    // every owner row this block reads (8b-TM+1 .. 8b+7) or the stream is zero
+                    if (8 * b - (TM - 1) > kzg[g][fcat] || kzs < 0 || k0 >= kend) continue;
+                    const int vb = V * NB + b;
+                    const int kf = kfs[vb], kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
+                    const double xo = xs[o], xo1 = xs[o + 1], iwo = iw[o];
+                    const double2 *sa = sb + static_cast<size_t>(b) * KCS * 32 + lane;
+                    // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
+                    // Z[t]: gain of owner rows o-t into rows o (gather form, far cells excluded)
+                    double L[NT][2], Xf[NT][2], Yf[NT][2], Z[TM][NT][2];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -483,16 +495,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 #pragma unroll
                             for (int t = 0; t < TM; ++t) Z[t][nt][e] = 0.0;
                         }
-                }
-                mbar_wait(&mbar[buf], (m / NST) & 1u);
-                if (!skip) {
-                    const double2 *sb = stg + static_cast<size_t>(buf) * SE;
-                    const double2 *sa = sb + static_cast<size_t>(b) * KCS * 32 + lane;
-                    const int k0 = cur.ch * KCS;
-                    const int kend = min(KS, min(k0 + KCS, (kzs >> 2) + 1));
-                    const int vb = V * NB + b;
-                    const int kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
-                    // B fragments (and w-scaled copies for a straddling group)
                     auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
@@ -572,29 +574,43 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         loadb(ks, bv, bw);
                         loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
                     }
-                    if (cur.ch == nchp - 1) { // pass complete: emission
-                        DgAcc Lv, Hv;
+                    // emission of this chunk's partial sums (linear): deltas in TMEM, dt at the apply
+                    double lv[4], hv[4];
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt)
+                    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int q = qg + 8 * nt + 2 * lc + e;
-                                const double f = on[nt][e] ? W(fcat, o, q) : 0.0; // dt: at the apply
-                                Lv[nt][e] = f * (L[nt][e] + Xf[nt][e]);
-                                const double hi = f * (Xf[nt][e] - Yf[nt][e]); // far cells -> row o+1
-                                const double up = __shfl_up_sync(0xffffffffu, hi, 4);
-                                double h = f * (Yf[nt][e] + Z[0][nt][e]);
-                                if (lr > 0) h += up;
-                                if (lr == 7) carry[(static_cast<size_t>(pd) * NB + b) * NP + q] += hi;
+                        for (int e = 0; e < 2; ++e) {
+                            const int q = qg + 8 * nt + 2 * lc + e;
+                            const double f = on[nt][e] ? W(fcat, o, q) : 0.0;
+                            lv[2 * nt + e] = f * (L[nt][e] + Xf[nt][e]);
+                            const double hi = f * (Xf[nt][e] - Yf[nt][e]); // far cells -> row o+1
+                            const double up = __shfl_up_sync(0xffffffffu, hi, 4);
+                            double h = f * (Yf[nt][e] + Z[0][nt][e]);
+                            if (lr > 0) h += up;
+                            if (lr == 7 && b + 1 < NB) carry[(static_cast<size_t>(pd) * NB + b) * NP + q] += hi;
 #pragma unroll
-                                for (int t = 1; t < TM; ++t) {
-                                    const int ot = o - t;
-                                    const double ft = on[nt][e] && ot >= 0 ? W(fcat, ot, q) : 0.0;
-                                    h = fma(ft, Z[t][nt][e], h);
-                                }
-                                Hv[nt][e] = h;
+                            for (int t = 1; t < TM; ++t) {
+                                const int ot = o - t;
+                                const double ft = on[nt][e] && ot >= 0 ? W(fcat, ot, q) : 0.0;
+                                h = fma(ft, Z[t][nt][e], h);
                             }
-                        emitg_switch(fcat * kNCat + pd, D, Lv, Hv);
+                            hv[2 * nt + e] = h;
+                        }
+                    const uint32_t ta = tmw + j * 48, tf = ta + 8 * fcat, tp = ta + 8 * pd;
+                    double d[4];
+                    tm_ld4(tf, d);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) d[i] -= lv[i];
+                    if (fcat == pd) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d[i] += hv[i];
+                        tm_st4(tf, d);
+                    } else {
+                        tm_st4(tf, d);
+                        tm_ld4(tp, d);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d[i] += hv[i];
+                        tm_st4(tp, d);
                     }
                 }
                 // release buffer `buf`; the last warp out refills it NST stages ahead
@@ -619,14 +635,21 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
             pbase += n;
             // ---- Jacobi apply (coalescence.cpp:313-328): own rows, then the block-head carries ----
             __syncthreads();
+            for (int j = 0; j < nbw; ++j) {
+                const int o = 8 * (j == 0 ? pw : NB - 1 - pw) + lr;
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
+                for (int c = 0; c < kNCat; ++c) {
+                    double d[4];
+                    tm_ld4(tmw + j * 48 + 8 * c, d);
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int q = qg + 8 * nt + 2 * lc + e;
+                    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int c = 0; c < kNCat; ++c) W(c, o, q) = fma(dt, D[c][nt][e], W(c, o, q));
+                        for (int e = 0; e < 2; ++e) {
+                            const int q = qg + 8 * nt + 2 * lc + e;
+                            W(c, o, q) = fma(dt, d[2 * nt + e], W(c, o, q));
+                        }
                 }
+            }
             __syncthreads();
             for (int f = tid; f < kNCat * (NB - 1) * NP; f += nthr) {
                 const int q = f % NP, cb = f / NP, c = cb / (NB - 1), bb = cb % (NB - 1);
@@ -662,21 +685,22 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
         }
         for (int q = tid; q < NP; q += nthr) {
             if (pidx[q] == 0xffffffffu || pfail[q] != 0) continue;
-            tr_acc += ptrip[q];
-            pt_acc += 1;
-            ev_acc += A.kernel_strategy ? ptrip[q] : full_evals;
+            atomicAdd(&cnt_sh[0], ptrip[q]);
+            atomicAdd(&cnt_sh[1], 1ull);
+            atomicAdd(&cnt_sh[2], A.kernel_strategy ? ptrip[q] : full_evals);
         }
         __syncthreads();
     }
-    for (int of = 16; of > 0; of >>= 1) {
-        tr_acc += __shfl_down_sync(0xffffffffu, tr_acc, of);
-        pt_acc += __shfl_down_sync(0xffffffffu, pt_acc, of);
-        ev_acc += __shfl_down_sync(0xffffffffu, ev_acc, of);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
-    if (lane == 0 && (tr_acc | pt_acc | ev_acc)) {
-        atomicAdd(&A.counters[0], tr_acc);
-        atomicAdd(&A.counters[1], pt_acc);
-        atomicAdd(&A.counters[2], ev_acc);
+    if (tid == 0 && (cnt_sh[0] | cnt_sh[1] | cnt_sh[2])) {
+        atomicAdd(&A.counters[0], cnt_sh[0]);
+        atomicAdd(&A.counters[1], cnt_sh[1]);
+        atomicAdd(&A.counters[2], cnt_sh[2]);
     }
 }
 
@@ -690,7 +714,7 @@ inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP) {
 template <int TM, int G, int MAXW>
 inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
     constexpr int NP = G * 16;
-    if (T.nblk * G > MAXW) return -1;
+    if ((T.nblk + 1) / 2 * G > MAXW) return -1;
     const size_t smem = dmmag_smem_bytes(T, NP);
     if (smem > 227 * 1024) return -1;
     DmmagArgs F{};
@@ -716,7 +740,7 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
         return 6;
     }
     const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
-    kern<<<grid, T.nblk * G * 32, smem, s>>>(A, F);
+    kern<<<grid, (T.nblk + 1) / 2 * G * 32, smem, s>>>(A, F);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fast_err() = std::string("dmmag path launch: ") + cudaGetErrorString(e);
@@ -725,10 +749,22 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     return 0;
 }
 
-/// Returns -1 when this geometry cannot run the general DMMA path.  One CTA of nblk
-/// warps (<= 12 so the register file allows 168 per thread) per 16-point batch.
+/// Returns -1 when this geometry cannot run the general DMMA path.  One CTA per batch
+/// of 32 points (2 point groups) when the spectra fit in shared memory, else 16 points;
+/// ceil(nblk/2) warps per group, each owning a balanced block pair.
 inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
-    if (!T.stages || A.nkr != T.nkr || T.nblk > 12) return -1;
+    if (!T.stages || A.nkr != T.nkr) return -1;
+    const int nwp = (T.nblk + 1) / 2;
+    if (2 * nwp <= 16 && dmmag_smem_bytes(T, 32) <= 227 * 1024) {
+        switch (T.TM) {
+        case 2: return launch_dmmag_t<2, 2, 16>(T, A, num_sms, s);
+        case 4: return launch_dmmag_t<4, 2, 16>(T, A, num_sms, s);
+        case 6: return launch_dmmag_t<6, 2, 16>(T, A, num_sms, s);
+        case 10: return launch_dmmag_t<10, 2, 16>(T, A, num_sms, s);
+        default: return -1;
+        }
+    }
+    if (nwp > 12) return -1;
     switch (T.TM) {
     case 2: return launch_dmmag_t<2, 1, 12>(T, A, num_sms, s);
     case 4: return launch_dmmag_t<4, 1, 12>(T, A, num_sms, s);
@@ -736,6 +772,14 @@ inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cu
     case 10: return launch_dmmag_t<10, 1, 12>(T, A, num_sms, s);
     default: return -1;
     }
+}
+
+/// Whether launch_dmmag takes this context's grid (same envelope, no launch).
+inline bool dmmag_supported(const DmmagTables &T) {
+    if (!T.stages) return false;
+    const int nwp = (T.nblk + 1) / 2;
+    return (2 * nwp <= 16 && dmmag_smem_bytes(T, 32) <= 227 * 1024) ||
+           (nwp <= 12 && dmmag_smem_bytes(T, 16) <= 227 * 1024);
 }
 
 } // namespace fsbm

@@ -925,7 +925,7 @@ int fsbm_probe_fp64_peak(int device, double *tflops) {
 int fsbm_ctx_fast_kernel(const fsbm_ctx *c, int *kernel) {
     if (!c || !kernel) return fail(FSBM_DOMAIN, "null context");
     const bool dm = c->dmma.blob && c->dmma.nkr == c->nkr;
-    const bool dg = c->dmmag.stages && c->dmmag.nkr == c->nkr && c->dmmag.nblk <= 12;
+    const bool dg = c->dmmag.nkr == c->nkr && dmmag_supported(c->dmmag);
     switch (c->fast_kernel) {
     case 1: *kernel = 1; break;
     case 2: *kernel = dm ? 2 : 0; break;

@@ -20,7 +20,7 @@ def forced(monkeypatch):
     monkeypatch.setenv("FSBM_FAST_KERNEL", "dmmag")
 
 
-@pytest.mark.parametrize("nkr", [17, 66])
+@pytest.mark.parametrize("nkr", [17, 66, 132])
 def test_default_dispatch_picks_dmmag(nkr):
     ctx, _, _ = make_ctx(nkr)
     assert ctx.fast_kernel() == "coal_dmmag"
@@ -34,7 +34,9 @@ def test_default_dispatch_picks_dmmag(nkr):
     (66, None, "levels", (2, 5, 33)),
     (66, None, "random", (2, 3, 21)),
     (48, 1.35, "levels", (2, 4, 17)),  # wider band (targets up to o+5)
-    (90, None, "levels", (1, 3, 17)),  # 12 blocks, the largest single-CTA grid
+    (90, None, "levels", (1, 3, 17)),  # 12 blocks: 16-point batches (shared-memory fit)
+    (132, None, "levels", (1, 2, 19)), # 17 blocks, targets up to o+5
+    (132, None, "random", (1, 2, 13)),
 ])
 def test_dmmag_vs_oracle(oracle, forced, nkr, ratio, pmode, dims):
     ctx, grid, tabs = make_ctx(nkr, ratio=ratio)
