@@ -43,14 +43,12 @@
 
 namespace fsbm {
 
-constexpr int kGNST = 3;     // table-stage ring depth
 constexpr int kGNT = 2;      // 8-point N-tiles per warp (16 points per group)
 
 struct DmmagTables {
-    int nkr = 0, S = 0, KS = 0, nblk = 0, SR = 0, KCS = 0, NCH = 0, TM = 0, npairs = 0;
+    int nkr = 0, S = 0, KS = 0, nblk = 0, SR = 0, TM = 0, npairs = 0;
     int item_base[kMaxPairs] = {};
-    size_t stage_elems = 0;      // double2 per stage = nblk * KCS * 32
-    double2 *stages = nullptr;   // [item][chunk][block][KCS][32]
+    double2 *stages = nullptr;   // [item][block][KS][32] A fragments (K500, Kd)
     double *consts = nullptr;    // x[SR+8] | invw[SR+8] (padded, finite)
     int *cls = nullptr;          // [3 views][nblk] leading far K-steps kf
     uint16_t *bmask = nullptr;   // [3 views][nblk][KS] gather target-offset masks
@@ -166,33 +164,29 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
             kg[(V * nblk + b) * 2 + 1] = kgh;
         }
     if (gco.empty()) gco.assign(32, 0.0);
-    // ---- per-pass A fragments, K-chunked ----
-    const int KCS = nblk <= 9 ? 6 : nblk <= 12 ? 4 : 3;
-    const int NCH = (KS + KCS - 1) / KCS;
-    const size_t stage_elems = static_cast<size_t>(nblk) * KCS * 32;
+    // ---- per-pass A fragments: [item][block][ks][lane] (K500, K750-K500) ----
     int nitems = 0;
     for (int p = 0; p < npairs; ++p) {
         D.item_base[p] = nitems;
         nitems += abd[3 * p] == abd[3 * p + 1] ? 1 : 2;
     }
-    std::vector<double2> st(static_cast<size_t>(nitems) * NCH * stage_elems, double2{0.0, 0.0});
+    const size_t item_elems = static_cast<size_t>(nblk) * KS * 32;
+    std::vector<double2> st(static_cast<size_t>(nitems) * item_elems, double2{0.0, 0.0});
     const size_t sq = static_cast<size_t>(nkr) * nkr;
     for (int p = 0; p < npairs; ++p) {
         const bool self = abd[3 * p] == abd[3 * p + 1];
         const double *k750 = t750 + p * sq, *k500 = t500 + p * sq;
         for (int X = 0; X < (self ? 1 : 2); ++X) {
-            double2 *base = st.data() + static_cast<size_t>(D.item_base[p] + X) * NCH * stage_elems;
-            for (int b = 0; b < nblk; ++b)
-                for (int ks = 0; ks < NCH * KCS; ++ks)
+            double2 *base = st.data() + static_cast<size_t>(D.item_base[p] + X) * item_elems;
+            for (int bb = 0; bb < nblk; ++bb)
+                for (int ks = 0; ks < KS; ++ks)
                     for (int lane = 0; lane < 32; ++lane) {
-                        const int o = 8 * b + (lane >> 2), s = 4 * ks + (lane & 3);
+                        const int o = 8 * bb + (lane >> 2), s = 4 * ks + (lane & 3);
                         if (o >= nkr || s >= nkr) continue;
                         const int i = X == 0 ? o : s, j = X == 0 ? s : o; // reference cell (i,j)
                         const size_t u = self ? static_cast<size_t>(std::min(i, j)) * nkr + std::max(i, j)
                                               : static_cast<size_t>(i) * nkr + j;
-                        const int ch = ks / KCS, kl = ks % KCS;
-                        base[static_cast<size_t>(ch) * stage_elems + (static_cast<size_t>(b) * KCS + kl) * 32 + lane] =
-                            double2{k500[u], k750[u] - k500[u]};
+                        base[(static_cast<size_t>(bb) * KS + ks) * 32 + lane] = double2{k500[u], k750[u] - k500[u]};
                     }
         }
     }
@@ -215,17 +209,15 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
     D.KS = KS;
     D.nblk = nblk;
     D.SR = SR;
-    D.KCS = KCS;
-    D.NCH = NCH;
     D.TM = TM;
     D.npairs = npairs;
-    D.stage_elems = stage_elems;
     return 0;
 }
 
 struct DmmagArgs {
-    int KS, nblk, SR, KCS, NCH;
-    uint32_t nbatches, stage_elems;
+    int KS, nblk, SR;
+    uint32_t nbatches;
+    int noskip;
     int item_base[kMaxPairs];
     const double2 *stages;
     const double *consts;
@@ -234,19 +226,20 @@ struct DmmagArgs {
     const double *gcoef;
 };
 
-typedef double DgAcc[kGNT][2];
-
 // ---- TMEM as the delta store (tcgen05.ld/st, 32x32b shape: thread i <-> TMEM lane base+i) ----
-__device__ __forceinline__ void tm_ld4(uint32_t taddr, double (&v)[4]) {
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+/// tcgen05.ld without the wait: the registers are valid only after tm_wait_ld().
+__device__ __forceinline__ void tm_ld4_nowait(uint32_t taddr, double (&v)[4]) {
     uint32_t r[8];
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                 : "r"(taddr)
+                 : "memory");
 #pragma unroll
     for (int i = 0; i < 4; ++i) v[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
 }
-__device__ __forceinline__ void tm_st4(uint32_t taddr, const double (&v)[4]) {
+__device__ __forceinline__ void tm_st4_nowait(uint32_t taddr, const double (&v)[4]) {
     uint32_t r[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -256,63 +249,64 @@ __device__ __forceinline__ void tm_st4(uint32_t taddr, const double (&v)[4]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-/// Position in the CTA's stage sequence: pass (pair p, X = 0 row / 1 column), K-chunk ch.
-struct GStage {
-    int p, X, ch;
-};
+constexpr int kGSlotCols = 48; // TMEM columns of one (group, block) delta slot: 6 categories x 4 doubles
 
-constexpr int kGTmemCols = 96; // per warp: 2 blocks x 6 categories x 4 doubles (2 columns each)
-
+/// Work unit = (pass, point group g, row block b), index i = b*G + g.  Unit i's deltas live
+/// in TMEM lane quadrant i % 4, slot i / 4: only that quadrant's warps can reach the slot,
+/// and they take the quadrant's units dynamically, in pass order, from one atomic counter.
 template <int TM, int G, int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, DmmagArgs F) {
-    constexpr int NT = kGNT, NP = G * 16, NST = kGNST;
+    constexpr int NT = kGNT, NP = G * 16;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nkr = A.nkr, SR = F.SR, KS = F.KS, KCS = F.KCS, NCH = F.NCH, NB = F.nblk;
-    const int NWP = (NB + 1) / 2; // warps per point group: one balanced block pair each
-    const uint32_t SE = F.stage_elems;
-    double2 *stg = reinterpret_cast<double2 *>(smem_raw);                          // [NST][SE]
-    double *work = reinterpret_cast<double *>(stg + NST * static_cast<size_t>(SE)); // [6][SR][NP]
-    double *carry = work + static_cast<size_t>(kNCat) * SR * NP;                  // [6][NB][NP]
-    double *xs = carry + static_cast<size_t>(kNCat) * NB * NP;                     // [SR+8]
-    double *iw = xs + SR + 8;                                                       // [SR+8]
-    double *wts = iw + SR + 8;                                                      // [NP]
-    unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP);     // [NP]
-    unsigned long long *ptrip = act + NP;                                           // [NP]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);                      // [NST]
-    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + NST);                      // [NP]
-    int *pfail = reinterpret_cast<int *>(pidx + NP);                                // [NP]
-    int *kfs = pfail + NP;                                                          // [3][NB]
-    int *kgs = kfs + 3 * NB;                                                        // [3][NB][2]
-    int *gofs = kgs + 6 * NB;                                                       // [3][NB][KS]
-    uint16_t *bms = reinterpret_cast<uint16_t *>(gofs + 3 * NB * KS);               // [3][NB][KS]
+    const int nkr = A.nkr, SR = F.SR, KS = F.KS, NB = F.nblk;
+    const int npairs = A.pairs.npairs, MP = 2 * npairs; // passes per substep (upper bound)
+    double *work = reinterpret_cast<double *>(smem_raw);                     // [6][SR][NP]
+    double *carry = work + static_cast<size_t>(kNCat) * SR * NP;             // [6][G][NB][16]
+    double *xs = carry + static_cast<size_t>(kNCat) * NB * NP;               // [SR+8]
+    double *iw = xs + SR + 8;                                                 // [SR+8]
+    double *wts = iw + SR + 8;                                                // [NP]
+    unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP); // [NP]
+    unsigned long long *ptrip = act + NP;                                     // [NP]
+    uint32_t *pidx = reinterpret_cast<uint32_t *>(ptrip + NP);                // [NP]
+    int *pfail = reinterpret_cast<int *>(pidx + NP);                          // [NP]
+    int *kfs = pfail + NP;                                                    // [3][NB]
+    int *kgs = kfs + 3 * NB;                                                  // [3][NB][2]
+    int *gofs = kgs + 6 * NB;                                                 // [3][NB][KS]
+    int *ps = gofs + 3 * NB * KS;                                             // [MP] pass: p | X<<8 | nlive<<16
+    int *pcum = ps + MP;                                                      // [4][MP+1] units per quadrant
+    int *served = pcum + 4 * (MP + 1);                                        // [G][NB] emitted units
+    uint16_t *rnk = reinterpret_cast<uint16_t *>(served + G * NB);            // [MP][NB] emission rank
+    uint16_t *bms = rnk + MP * NB;                                            // [3][NB][KS]
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
     __shared__ int kzc[kNCat];
-    __shared__ int relcnt[NST];
+    __shared__ int qcnt[4];
+    __shared__ int npass;
     __shared__ uint32_t tmem_base;
     __shared__ unsigned long long cnt_sh[3];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
     const int wid = tid >> 5, lane = tid & 31;
-    const int g = wid / NWP, pw = wid % NWP;
-    const int nbw = pw == NB - 1 - pw ? 1 : 2;          // blocks owned by this warp
+    const int quad = wid & 3, wqi = wid >> 2, nq = (NW - quad + 3) >> 2;
     const int lr = lane >> 2, lc = lane & 3;
-    const int qg = g * 16;
     if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const uint32_t nact = *A.nactive;
-    const int npairs = A.pairs.npairs;
     const unsigned long long full_evals = static_cast<unsigned long long>(npairs) * nkr * nkr;
     const int self_tri = nkr * (nkr + 1) / 2, cross_sq = nkr * nkr;
     const double dt = A.dt_sub;
-    const uint32_t sbytes = SE * static_cast<uint32_t>(sizeof(double2));
+    const int nslots = (NB * G - 1) / 4 + 1; // slots per quadrant
 
     // point-minor spectra, bit 3 of the point index swizzled by the bin's parity: the
     // four K rows of a B fragment (8 points each) then hit disjoint bank halves
     auto W = [&](int c, int s, int q) -> double & {
         return work[(static_cast<size_t>(c) * SR + s) * NP + (q ^ ((s & 1) << 3))];
+    };
+    auto CR = [&](int c, int g, int b, int q) -> double & {
+        return carry[((static_cast<size_t>(c) * G + g) * NB + b) * 16 + q];
     };
 
     for (int f = tid; f < 2 * (SR + 8); f += nthr) xs[f] = F.consts[f];
@@ -324,20 +318,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     }
     for (int f = tid; f < kNCat * SR * NP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
     if (tid < 3) cnt_sh[tid] = 0ull;
-    if (tid == 0) {
-        for (int i = 0; i < NST; ++i) mbar_init(&mbar[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (wid == 0) { // the whole TMEM of the SM: deltas of every warp's blocks
+    if (wid == 0) { // TMEM (whole SM): the delta slots of every (group, block)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    tm_fence_before();
     __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this warp's delta columns: lanes 32*(wid%4).., columns (wid/4)*96 + j*48 + c*8
-    const uint32_t tmw = tmem_base + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + (wid >> 2) * kGTmemCols;
-    uint32_t pbase = 0;
+    tm_fence_after();
+    const uint32_t tmq = tmem_base + (static_cast<uint32_t>(32 * quad) << 16); // this warp's lane quadrant
 
     for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
          batch += gridDim.x) {
@@ -368,13 +356,18 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
             if (tid == 0) cta_act = 0ull;
             if (tid < G * kNCat) kzg[tid / kNCat][tid % kNCat] = -1;
             if (tid < kNCat) kzc[tid] = -1;
-            if (tid < NST) relcnt[tid] = 0;
+            if (tid < 4) qcnt[tid] = 0;
+            for (int f = tid; f < G * NB; f += nthr) served[f] = 0;
             for (int f = tid; f < kNCat * NB * NP; f += nthr) carry[f] = 0.0;
-            {
+            { // zero this warp's share of its quadrant's delta slots
                 const double z[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int k = 0; k < 2 * kNCat; ++k) tm_st4(tmw + 8 * k, z);
+                for (int k = wqi; k < nslots; k += nq)
+                    for (int c = 0; c < kNCat; ++c) tm_st4_nowait(tmq + k * kGSlotCols + 8 * c, z);
+                tm_wait_st();
             }
+            tm_fence_before();
             __syncthreads();
+            tm_fence_after();
             for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
                 unsigned nz = 0;
                 for (int c = 0; c < kNCat; ++c) { // scanned from the top: last non-zero bin
@@ -382,8 +375,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     while (l >= 0 && W(c, l, q) == 0.0) --l;
                     nz |= l >= 0 ? (1u << c) : 0u;
                     if (l >= 0 && pfail[q] == 0) {
-                        atomicMax(&kzg[q / 16][c], l);
-                        atomicMax(&kzc[c], l);
+                        const int lk = F.noskip ? nkr - 1 : l; // A/B: FSBM_DMMAG_NOSKIP
+                        atomicMax(&kzg[q / 16][c], lk);
+                        atomicMax(&kzc[c], lk);
                     }
                 }
                 unsigned long long m = 0, trip = 0;
@@ -401,89 +395,76 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 }
             }
             __syncthreads();
-            const unsigned long long amask = cta_act;
-
-            // ---- the CTA's stage sequence (identical in every warp) ----
-            auto pass_nch = [&](int p, int X) -> int {
-                const int pa = A.pairs.a[p], pb = A.pairs.b[p];
-                const int fc = X == 0 ? pa : pb, sc = X == 0 ? pb : pa;
-                if (kzc[fc] < 0 || kzc[sc] < 0) return 0; // every product of the pass is zero
-                return min(NCH, kzc[sc] / (4 * KCS) + 1);
-            };
-            auto advance = [&](GStage s) -> GStage { // next stage strictly after s
-                if (s.p < 0) return s;
-                if (s.ch + 1 < pass_nch(s.p, s.X)) return GStage{s.p, s.X, s.ch + 1};
-                int p = s.p, X = s.X;
-                while (true) {
-                    ++X;
-                    if (X > (A.pairs.a[p] == A.pairs.b[p] ? 0 : 1)) {
-                        const unsigned long long rest = amask & ~((2ull << p) - 1ull);
-                        if (!rest) return GStage{-1, 0, 0};
-                        p = __ffsll(static_cast<long long>(rest)) - 1;
-                        X = 0;
+            if (tid == 0) { // the pass sequence, its units per quadrant and the emission ranks
+                const unsigned long long amask = cta_act;
+                int np_ = 0, cum[4] = {0, 0, 0, 0};
+                for (int k = 0; k < 4; ++k) pcum[k * (MP + 1)] = 0;
+                for (int p = 0; p < npairs; ++p) {
+                    if (!(amask >> p & 1ull)) continue;
+                    const int pa = A.pairs.a[p], pb = A.pairs.b[p];
+                    for (int X = 0; X < (pa == pb ? 1 : 2); ++X) {
+                        const int fc = X == 0 ? pa : pb, sc = X == 0 ? pb : pa;
+                        if (kzc[fc] < 0 || kzc[sc] < 0) continue; // every product of the pass is zero
+                        const int nl = min(NB, (kzc[fc] + TM - 1) / 8 + 1);
+                        for (int b = 0; b < NB; ++b) {
+                            int r = 0;
+                            for (int i = 0; i < np_; ++i) r += (ps[i] >> 16) > b ? 1 : 0;
+                            rnk[np_ * NB + b] = static_cast<uint16_t>(r);
+                        }
+                        ps[np_] = p | X << 8 | nl << 16;
+                        for (int i = 0; i < nl * G; ++i) ++cum[i & 3];
+                        ++np_;
+                        for (int k = 0; k < 4; ++k) pcum[k * (MP + 1) + np_] = cum[k];
                     }
-                    if (pass_nch(p, X) > 0) return GStage{p, X, 0};
                 }
-            };
-            auto issue = [&](GStage s, int buf) {
-                mbar_expect_tx(&mbar[buf], sbytes);
-                const size_t off = (static_cast<size_t>(F.item_base[s.p] + s.X) * NCH + s.ch) * SE;
-                tma_bulk_g2s(stg + static_cast<size_t>(buf) * SE, F.stages + off, sbytes, &mbar[buf]);
-            };
-            GStage cur{-1, 0, 0};
-            if (amask) {
-                const int p0 = __ffsll(static_cast<long long>(amask)) - 1;
-                cur = pass_nch(p0, 0) > 0 ? GStage{p0, 0, 0} : advance(GStage{p0, 0, NCH});
-            }
-            if (tid == 0) { // prime the ring
-                fence_proxy_async();
-                GStage s = cur;
-                for (int i = 0; i < NST && s.p >= 0; ++i, s = advance(s)) issue(s, (pbase + i) % NST);
+                npass = np_;
             }
             __syncthreads();
 
-            int fcat = 0, scat = 0, pd = 0, V = 0, kzs = -1;
-            bool uni = true;
-            double wu = 0.0, wq[NT] = {0.0, 0.0};
-            bool on[NT][2];
-            int n = 0;
-            while (cur.p >= 0) {
-                const uint32_t m = pbase + n;
-                const int buf = m % NST;
-                if (cur.ch == 0) {
-                    const int pa = A.pairs.a[cur.p], pb = A.pairs.b[cur.p];
-                    fcat = cur.X == 0 ? pa : pb;
-                    scat = cur.X == 0 ? pb : pa;
-                    pd = A.pairs.d[cur.p];
-                    V = cur.X == 1 ? 2 : (pa == pb ? 1 : 0);
-                    kzs = kzg[g][scat];
-                    wu = wts[qg];
-                    bool allu = true;
+            // ---- units: dynamic within the lane quadrant, pass order ----
+            const int NPS = npass;
+            const int *pc = pcum + quad * (MP + 1);
+            int pi = 0;
+            while (true) {
+                int u = 0;
+                if (lane == 0) u = atomicAdd(&qcnt[quad], 1);
+                u = __shfl_sync(0xffffffffu, u, 0);
+                while (pi < NPS && u >= pc[pi + 1]) ++pi;
+                if (pi >= NPS) break;
+                const int pw_ = ps[pi], p = pw_ & 255, X = (pw_ >> 8) & 255, nl = pw_ >> 16;
+                const int iu = quad + 4 * (u - pc[pi]); // unit index b*G + g within the pass
+                const int b = iu / G, g = iu % G;
+                const int slot = iu >> 2;
+                const int rank = rnk[pi * NB + b];
+                const int pa = A.pairs.a[p], pb = A.pairs.b[p];
+                const int fcat = X == 0 ? pa : pb, scat = X == 0 ? pb : pa, pd = A.pairs.d[p];
+                const int V = X == 1 ? 2 : (pa == pb ? 1 : 0);
+                const int kzs = kzg[g][scat];
+                const int qg = 16 * g, o = 8 * b + lr;
+                // every owner row this unit reads (8b-TM+1 .. 8b+7) or the stream is zero
+                const bool live = 8 * b - (TM - 1) <= kzg[g][fcat] && kzs >= 0;
+                double lv[4] = {0.0, 0.0, 0.0, 0.0}, hv[4] = {0.0, 0.0, 0.0, 0.0};
+                if (live) {
+                    bool on[NT][2], allu = true;
+                    double wq[NT];
+                    const double wu = wts[qg];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
                         wq[nt] = wts[qg + 8 * nt + lr];
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int q = qg + 8 * nt + 2 * lc + e;
-                            on[nt][e] = act[q] >> cur.p & 1ull;
+                            on[nt][e] = act[q] >> p & 1ull;
                             allu = allu && wts[q] == wu;
                         }
                     }
-                    uni = __all_sync(0xffffffffu, allu);
-                }
-                mbar_wait(&mbar[buf], (m / NST) & 1u);
-                const double2 *sb = stg + static_cast<size_t>(buf) * SE;
-                const int k0 = cur.ch * KCS;
-                const int kend = min(KS, min(k0 + KCS, (kzs >> 2) + 1));
-                for (int j = 0; j < nbw; ++j) {
-                    const int b = j == 0 ? pw : NB - 1 - pw;
-                    const int o = 8 * b + lr;
-                    // every owner row this block reads (8b-TM+1 .. 8b+7) or the stream is zero
-                    if (8 * b - (TM - 1) > kzg[g][fcat] || kzs < 0 || k0 >= kend) continue;
+                    const bool uni = __all_sync(0xffffffffu, allu);
                     const int vb = V * NB + b;
                     const int kf = kfs[vb], kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
+                    const int kend = min(KS, (kzs >> 2) + 1);
                     const double xo = xs[o], xo1 = xs[o + 1], iwo = iw[o];
-                    const double2 *sa = sb + static_cast<size_t>(b) * KCS * 32 + lane;
+                    const double2 *gi = F.stages + static_cast<size_t>(F.item_base[p] + X) * NB * KS * 32;
+                    const double2 *ga = gi + static_cast<size_t>(b) * KS * 32 + lane;
                     // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
                     // Z[t]: gain of owner rows o-t into rows o (gather form, far cells excluded)
                     double L[NT][2], Xf[NT][2], Yf[NT][2], Z[TM][NT][2];
@@ -522,18 +503,18 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
                         }
                     };
-                    int ks = k0;
+                    int ks = 0;
                     // (1) far steps before any gather entry
-#pragma unroll 2
+#pragma unroll 4
                     for (; ks < min(kend, min(kf, kgl)); ++ks) {
-                        const double2 kk = sa[(ks - k0) * 32];
+                        const double2 kk = __ldg(ga + ks * 32);
                         double bv[NT], bw[NT];
                         loadb(ks, bv, bw);
                         far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
                     }
                     // (2) general steps: far or loss, plus the gather entries of the step
                     for (; ks < min(kend, max(kf, kgh)); ++ks) {
-                        const double2 kk = sa[(ks - k0) * 32];
+                        const double2 kk = __ldg(ga + ks * 32);
                         double bv[NT], bw[NT];
                         loadb(ks, bv, bw);
                         const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
@@ -551,8 +532,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                     double at = a, adt = ad;
                                     if (t > 0) {
                                         const int ot = max(o - t, 0); // rows < 0 carry c == 0
-                                        const double2 k2 = sb[static_cast<size_t>(ot >> 3) * KCS * 32 + (ks - k0) * 32 +
-                                                              (((ot & 7) << 2) | lc)];
+                                        const double2 k2 = __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
+                                                                 (((ot & 7) << 2) | lc));
                                         at = uni ? fma(wu, k2.y, k2.x) : k2.x;
                                         adt = k2.y;
                                     }
@@ -567,15 +548,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         }
                     }
                     // (3) loss-only steps above the band
-#pragma unroll 2
+#pragma unroll 4
                     for (; ks < kend; ++ks) {
-                        const double2 kk = sa[(ks - k0) * 32];
+                        const double2 kk = __ldg(ga + ks * 32);
                         double bv[NT], bw[NT];
                         loadb(ks, bv, bw);
                         loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
                     }
-                    // emission of this chunk's partial sums (linear): deltas in TMEM, dt at the apply
-                    double lv[4], hv[4];
+                    // owner emission values (dt at the apply); far-cell hi gains of row 7
+                    // carry into the next block's head row
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -583,78 +564,90 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             const int q = qg + 8 * nt + 2 * lc + e;
                             const double f = on[nt][e] ? W(fcat, o, q) : 0.0;
                             lv[2 * nt + e] = f * (L[nt][e] + Xf[nt][e]);
-                            const double hi = f * (Xf[nt][e] - Yf[nt][e]); // far cells -> row o+1
+                            const double hi = f * (Xf[nt][e] - Yf[nt][e]);
                             const double up = __shfl_up_sync(0xffffffffu, hi, 4);
                             double h = f * (Yf[nt][e] + Z[0][nt][e]);
                             if (lr > 0) h += up;
-                            if (lr == 7 && b + 1 < NB) carry[(static_cast<size_t>(pd) * NB + b) * NP + q] += hi;
+                            hv[2 * nt + e] = h;
+                            Xf[nt][e] = hi; // keep for the carry
 #pragma unroll
                             for (int t = 1; t < TM; ++t) {
                                 const int ot = o - t;
                                 const double ft = on[nt][e] && ot >= 0 ? W(fcat, ot, q) : 0.0;
-                                h = fma(ft, Z[t][nt][e], h);
+                                hv[2 * nt + e] = fma(ft, Z[t][nt][e], hv[2 * nt + e]);
                             }
-                            hv[2 * nt + e] = h;
                         }
-                    const uint32_t ta = tmw + j * 48, tf = ta + 8 * fcat, tp = ta + 8 * pd;
-                    double d[4];
-                    tm_ld4(tf, d);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) d[i] -= lv[i];
-                    if (fcat == pd) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) d[i] += hv[i];
-                        tm_st4(tf, d);
-                    } else {
-                        tm_st4(tf, d);
-                        tm_ld4(tp, d);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) d[i] += hv[i];
-                        tm_st4(tp, d);
-                    }
-                }
-                // release buffer `buf`; the last warp out refills it NST stages ahead
-                __syncwarp();
-                if (lane == 0) {
+                    // wait for this block's earlier units (deterministic accumulation order)
+                    if (lane == 0)
+                        while (*reinterpret_cast<volatile int *>(&served[g * NB + b]) != rank) {
+                        }
+                    __syncwarp();
                     __threadfence_block();
-                    const int old = atomicAdd(&relcnt[buf], 1);
-                    if (old == NW - 1) {
-                        relcnt[buf] = 0;
-                        __threadfence_block();
-                        GStage s2 = cur;
-                        for (int i = 0; i < NST; ++i) s2 = advance(s2);
-                        if (s2.p >= 0) {
-                            fence_proxy_async();
-                            issue(s2, buf);
+                    tm_fence_after();
+                    if (lr == 7 && b + 1 < NB) {
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) CR(pd, g, b, 8 * nt + 2 * lc + e) += Xf[nt][e];
+                    }
+                    const uint32_t ta = tmq + slot * kGSlotCols, tf = ta + 8 * fcat, tp = ta + 8 * pd;
+                    if (fcat == pd) {
+                        double d[4];
+                        tm_ld4_nowait(tf, d);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d[i] += hv[i] - lv[i];
+                        tm_st4_nowait(tf, d);
+                    } else {
+                        double d[4], e4[4];
+                        tm_ld4_nowait(tf, d);
+                        tm_ld4_nowait(tp, e4);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            d[i] -= lv[i];
+                            e4[i] += hv[i];
                         }
+                        tm_st4_nowait(tf, d);
+                        tm_st4_nowait(tp, e4);
+                    }
+                    tm_wait_st();
+                    tm_fence_before();
+                } else if (lane == 0) {
+                    while (*reinterpret_cast<volatile int *>(&served[g * NB + b]) != rank) {
                     }
                 }
-                cur = advance(cur);
-                ++n;
+                __syncwarp();
+                __threadfence_block();
+                if (lane == 0) *reinterpret_cast<volatile int *>(&served[g * NB + b]) = rank + 1;
             }
-            pbase += n;
             // ---- Jacobi apply (coalescence.cpp:313-328): own rows, then the block-head carries ----
+            tm_fence_before();
             __syncthreads();
-            for (int j = 0; j < nbw; ++j) {
-                const int o = 8 * (j == 0 ? pw : NB - 1 - pw) + lr;
+            tm_fence_after();
+            for (int k = wqi; k < nslots; k += nq)
+                {
+                    const int iu = 4 * k + quad, b = iu / G, g = iu % G;
+                    if (b >= NB) continue;
+                    const int o = 8 * b + lr;
 #pragma unroll
-                for (int c = 0; c < kNCat; ++c) {
-                    double d[4];
-                    tm_ld4(tmw + j * 48 + 8 * c, d);
+                    for (int c = 0; c < kNCat; ++c) {
+                        double d[4];
+                        tm_ld4_nowait(tmq + k * kGSlotCols + 8 * c, d);
+                        tm_wait_ld();
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
+                        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int q = qg + 8 * nt + 2 * lc + e;
-                            W(c, o, q) = fma(dt, d[2 * nt + e], W(c, o, q));
-                        }
+                            for (int e = 0; e < 2; ++e) {
+                                const int q = 16 * g + 8 * nt + 2 * lc + e;
+                                W(c, o, q) = fma(dt, d[2 * nt + e], W(c, o, q));
+                            }
+                    }
                 }
-            }
             __syncthreads();
-            for (int f = tid; f < kNCat * (NB - 1) * NP; f += nthr) {
-                const int q = f % NP, cb = f / NP, c = cb / (NB - 1), bb = cb % (NB - 1);
-                const int row = 8 * (bb + 1);
-                W(c, row, q) = fma(dt, carry[(static_cast<size_t>(c) * NB + bb) * NP + q], W(c, row, q));
+            for (int f = tid; f < kNCat * G * (NB - 1) * 16; f += nthr) {
+                const int q = f % 16, r = f / 16, bb = r % (NB - 1), cg = r / (NB - 1), g = cg % G, c = cg / G;
+                W(c, 8 * (bb + 1), 16 * g + q) = fma(dt, CR(c, g, bb, q), W(c, 8 * (bb + 1), 16 * g + q));
             }
             __syncthreads();
             for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
@@ -691,10 +684,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
         }
         __syncthreads();
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    tm_fence_before();
     __syncthreads();
     if (wid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tm_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
     if (tid == 0 && (cnt_sh[0] | cnt_sh[1] | cnt_sh[2])) {
@@ -704,27 +697,26 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     }
 }
 
+/// Shared memory of a launch with NP points per batch.
 inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP) {
-    return static_cast<size_t>(kGNST) * T.stage_elems * sizeof(double2) +
-           (static_cast<size_t>(kNCat) * T.SR * NP + static_cast<size_t>(kNCat) * T.nblk * NP + 2 * (T.SR + 8) + NP) *
+    const size_t MP = 2 * static_cast<size_t>(T.npairs);
+    return (static_cast<size_t>(kNCat) * T.SR * NP + static_cast<size_t>(kNCat) * T.nblk * NP + 2 * (T.SR + 8) + NP) *
                sizeof(double) +
-           NP * 16 + kGNST * 8 + NP * 8 + 9 * T.nblk * 4 + 3 * T.nblk * T.KS * 6 + 16;
+           NP * 16 + NP * 8 + 9 * T.nblk * 4 + 3 * T.nblk * T.KS * 6 + MP * 4 + 4 * (MP + 1) * 4 +
+           2 * T.nblk * 4 + MP * T.nblk * 2 + 16;
 }
 
 template <int TM, int G, int MAXW>
-inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
+inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s, int nwarps) {
     constexpr int NP = G * 16;
-    if ((T.nblk + 1) / 2 * G > MAXW) return -1;
     const size_t smem = dmmag_smem_bytes(T, NP);
-    if (smem > 227 * 1024) return -1;
+    if (smem > 227 * 1024 || nwarps > MAXW) return -1;
     DmmagArgs F{};
     F.KS = T.KS;
     F.nblk = T.nblk;
     F.SR = T.SR;
-    F.KCS = T.KCS;
-    F.NCH = T.NCH;
     F.nbatches = (A.nactive_host + NP - 1) / NP;
-    F.stage_elems = static_cast<uint32_t>(T.stage_elems);
+    F.noskip = std::getenv("FSBM_DMMAG_NOSKIP") != nullptr;
     for (int p = 0; p < kMaxPairs; ++p) F.item_base[p] = T.item_base[p];
     F.stages = T.stages;
     F.consts = T.consts;
@@ -740,7 +732,7 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
         return 6;
     }
     const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
-    kern<<<grid, (T.nblk + 1) / 2 * G * 32, smem, s>>>(A, F);
+    kern<<<grid, nwarps * 32, smem, s>>>(A, F);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fast_err() = std::string("dmmag path launch: ") + cudaGetErrorString(e);
@@ -749,37 +741,40 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     return 0;
 }
 
-/// Returns -1 when this geometry cannot run the general DMMA path.  One CTA per batch
-/// of 32 points (2 point groups) when the spectra fit in shared memory, else 16 points;
-/// ceil(nblk/2) warps per group, each owning a balanced block pair.
-inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
-    if (!T.stages || A.nkr != T.nkr) return -1;
-    const int nwp = (T.nblk + 1) / 2;
-    if (2 * nwp <= 16 && dmmag_smem_bytes(T, 32) <= 227 * 1024) {
-        switch (T.TM) {
-        case 2: return launch_dmmag_t<2, 2, 16>(T, A, num_sms, s);
-        case 4: return launch_dmmag_t<4, 2, 16>(T, A, num_sms, s);
-        case 6: return launch_dmmag_t<6, 2, 16>(T, A, num_sms, s);
-        case 10: return launch_dmmag_t<10, 2, 16>(T, A, num_sms, s);
-        default: return -1;
-        }
-    }
-    if (nwp > 12) return -1;
-    switch (T.TM) {
-    case 2: return launch_dmmag_t<2, 1, 12>(T, A, num_sms, s);
-    case 4: return launch_dmmag_t<4, 1, 12>(T, A, num_sms, s);
-    case 6: return launch_dmmag_t<6, 1, 12>(T, A, num_sms, s);
-    case 10: return launch_dmmag_t<10, 1, 12>(T, A, num_sms, s);
-    default: return -1;
-    }
+/// Point groups per batch: the most (<= 3) whose spectra fit in shared memory.
+inline int dmmag_groups(const DmmagTables &T) {
+    for (int G = 3; G >= 1; --G)
+        if (dmmag_smem_bytes(T, 16 * G) <= 227 * 1024) return G;
+    return 0;
 }
 
 /// Whether launch_dmmag takes this context's grid (same envelope, no launch).
 inline bool dmmag_supported(const DmmagTables &T) {
-    if (!T.stages) return false;
-    const int nwp = (T.nblk + 1) / 2;
-    return (2 * nwp <= 16 && dmmag_smem_bytes(T, 32) <= 227 * 1024) ||
-           (nwp <= 12 && dmmag_smem_bytes(T, 16) <= 227 * 1024);
+    const int G = dmmag_groups(T);
+    return T.stages && T.npairs <= kMaxPairs && G > 0 && (T.nblk * G - 1) / 4 + 1 <= 512 / kGSlotCols;
+}
+
+/// Returns -1 when this geometry cannot run the general DMMA path.  Warps: 16 (128
+/// registers) for target offsets <= 4, else 12 (168 registers); FSBM_DMMAG_WARPS overrides.
+inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
+    if (!T.stages || A.nkr != T.nkr || !dmmag_supported(T)) return -1;
+    const int G = dmmag_groups(T);
+    int nw = T.TM <= 4 ? 16 : 12;
+    if (const char *ev = std::getenv("FSBM_DMMAG_WARPS")) nw = std::max(4, std::min(nw, std::atoi(ev)));
+#define FSBM_DG(TM_, MW_)                                                                          \
+    switch (G) {                                                                                   \
+    case 3: return launch_dmmag_t<TM_, 3, MW_>(T, A, num_sms, s, nw);                              \
+    case 2: return launch_dmmag_t<TM_, 2, MW_>(T, A, num_sms, s, nw);                              \
+    default: return launch_dmmag_t<TM_, 1, MW_>(T, A, num_sms, s, nw);                             \
+    }
+    switch (T.TM) {
+    case 2: FSBM_DG(2, 16)
+    case 4: FSBM_DG(4, 16)
+    case 6: FSBM_DG(6, 12)
+    case 10: FSBM_DG(10, 12)
+    default: return -1;
+    }
+#undef FSBM_DG
 }
 
 } // namespace fsbm
