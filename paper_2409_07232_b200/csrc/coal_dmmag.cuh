@@ -395,29 +395,39 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 }
             }
             __syncthreads();
-            if (tid == 0) { // the pass sequence, its units per quadrant and the emission ranks
+            if (tid == 0) { // the pass sequence: p | X << 8 | live blocks << 16
                 const unsigned long long amask = cta_act;
-                int np_ = 0, cum[4] = {0, 0, 0, 0};
-                for (int k = 0; k < 4; ++k) pcum[k * (MP + 1)] = 0;
+                int np_ = 0;
                 for (int p = 0; p < npairs; ++p) {
                     if (!(amask >> p & 1ull)) continue;
                     const int pa = A.pairs.a[p], pb = A.pairs.b[p];
                     for (int X = 0; X < (pa == pb ? 1 : 2); ++X) {
                         const int fc = X == 0 ? pa : pb, sc = X == 0 ? pb : pa;
                         if (kzc[fc] < 0 || kzc[sc] < 0) continue; // every product of the pass is zero
-                        const int nl = min(NB, (kzc[fc] + TM - 1) / 8 + 1);
-                        for (int b = 0; b < NB; ++b) {
-                            int r = 0;
-                            for (int i = 0; i < np_; ++i) r += (ps[i] >> 16) > b ? 1 : 0;
-                            rnk[np_ * NB + b] = static_cast<uint16_t>(r);
-                        }
-                        ps[np_] = p | X << 8 | nl << 16;
-                        for (int i = 0; i < nl * G; ++i) ++cum[i & 3];
-                        ++np_;
-                        for (int k = 0; k < 4; ++k) pcum[k * (MP + 1) + np_] = cum[k];
+                        ps[np_++] = p | X << 8 | min(NB, (kzc[fc] + TM - 1) / 8 + 1) << 16;
                     }
                 }
                 npass = np_;
+            }
+            __syncthreads();
+            {
+                const int NPS = npass;
+                for (int b = tid; b < NB; b += nthr) { // emission rank: earlier passes with block b live
+                    int r = 0;
+                    for (int i = 0; i < NPS; ++i) {
+                        rnk[i * NB + b] = static_cast<uint16_t>(r);
+                        r += (ps[i] >> 16) > b ? 1 : 0;
+                    }
+                }
+                if (tid >= 32 && tid < 36) { // units per quadrant, prefix over passes
+                    const int q = tid - 32;
+                    int c = 0;
+                    pcum[q * (MP + 1)] = 0;
+                    for (int i = 0; i < NPS; ++i) {
+                        c += ((ps[i] >> 16) * G - q + 3) / 4;
+                        pcum[q * (MP + 1) + i + 1] = c;
+                    }
+                }
             }
             __syncthreads();
 
