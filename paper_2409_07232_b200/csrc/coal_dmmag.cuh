@@ -55,6 +55,7 @@ struct DmmagTables {
     int *goff = nullptr;         // [3][nblk][KS] first gather fragment of the step
     int *kg = nullptr;           // [3][nblk][2] K-step range holding gather entries
     double *gcoef = nullptr;     // [entry][32] gather weight fragments
+    double *carry_g = nullptr;   // [SMs][6][nblk][16] carry rows of lean (global) launches
 };
 
 inline void free_dmmag_tables(DmmagTables &t) {
@@ -65,6 +66,7 @@ inline void free_dmmag_tables(DmmagTables &t) {
     cudaFree(t.goff);
     cudaFree(t.kg);
     cudaFree(t.gcoef);
+    cudaFree(t.carry_g);
     t = DmmagTables{};
 }
 
@@ -75,7 +77,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                               const std::vector<int32_t> &g_lo, const std::vector<double> &g_wlo,
                               const std::vector<double> &g_whi, const std::vector<double> &g_top) {
     D = DmmagTables{};
-    if (nkr < 8 || nkr > 192) return 0;
+    if (nkr < 8 || nkr > 320) return 0;
     const int S = (nkr + 3) / 4 * 4, KS = S / 4, nblk = (nkr + 7) / 8, SR = nblk * 8;
     // far-cell weights are recomputed on the fly: c0 = (x[o+1] - (x[o] + x[s])) / width[o]
     // (one multiply by the reciprocal; checked against the GainTable per far cell below)
@@ -211,13 +213,24 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
     D.SR = SR;
     D.TM = TM;
     D.npairs = npairs;
+    if (nblk > 16) { // spectra of 16 points leave no room for the carry rows: global scratch per CTA
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaMalloc(&D.carry_g, static_cast<size_t>(sms) * kNCat * nblk * 16 * sizeof(double)) != cudaSuccess) {
+            free_dmmag_tables(D);
+            fast_err() = "dmmag tables: device allocation failed";
+            return 6;
+        }
+    }
     return 0;
 }
 
 struct DmmagArgs {
     int KS, nblk, SR;
     uint32_t nbatches;
-    int noskip;
+    int noskip, lean;
+    double *carry_g;
     int item_base[kMaxPairs];
     const double2 *stages;
     const double *consts;
@@ -264,9 +277,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nkr = A.nkr, SR = F.SR, KS = F.KS, NB = F.nblk;
     const int npairs = A.pairs.npairs, MP = 2 * npairs; // passes per substep (upper bound)
+    // shared-memory layout (dmmag_smem_bytes); the carry rows and the band tables move to
+    // global memory when the spectra leave no room (F.lean: 264-bin grids)
     double *work = reinterpret_cast<double *>(smem_raw);                     // [6][SR][NP]
-    double *carry = work + static_cast<size_t>(kNCat) * SR * NP;             // [6][G][NB][16]
-    double *xs = carry + static_cast<size_t>(kNCat) * NB * NP;               // [SR+8]
+    double *xs = work + static_cast<size_t>(kNCat) * SR * NP;                // [SR+8]
     double *iw = xs + SR + 8;                                                 // [SR+8]
     double *wts = iw + SR + 8;                                                // [NP]
     unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP); // [NP]
@@ -275,12 +289,32 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     int *pfail = reinterpret_cast<int *>(pidx + NP);                          // [NP]
     int *kfs = pfail + NP;                                                    // [3][NB]
     int *kgs = kfs + 3 * NB;                                                  // [3][NB][2]
-    int *gofs = kgs + 6 * NB;                                                 // [3][NB][KS]
-    int *ps = gofs + 3 * NB * KS;                                             // [MP] pass: p | X<<8 | nlive<<16
+    int *ps = kgs + 6 * NB;                                                   // [MP] pass: p | X<<8 | nlive<<16
     int *pcum = ps + MP;                                                      // [4][MP+1] units per quadrant
     int *served = pcum + 4 * (MP + 1);                                        // [G][NB] emitted units
     uint16_t *rnk = reinterpret_cast<uint16_t *>(served + G * NB);            // [MP][NB] emission rank
-    uint16_t *bms = rnk + MP * NB;                                            // [3][NB][KS]
+    double *carry;                                                            // [6][G][NB][16]
+    const int *gofs;                                                          // [3][NB][KS]
+    const uint16_t *bms;                                                      // [3][NB][KS]
+    {
+        unsigned char *tail = reinterpret_cast<unsigned char *>(rnk + MP * NB);
+        tail += (16 - reinterpret_cast<uintptr_t>(tail) % 16) % 16;
+        if (F.lean) {
+            carry = F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP;
+            gofs = F.goff;
+            bms = F.bmask;
+        } else {
+            carry = reinterpret_cast<double *>(tail);
+            int *g2 = reinterpret_cast<int *>(carry + static_cast<size_t>(kNCat) * NB * NP);
+            uint16_t *b2 = reinterpret_cast<uint16_t *>(g2 + 3 * NB * KS);
+            for (int f = threadIdx.x; f < 3 * NB * KS; f += blockDim.x) {
+                g2[f] = F.goff[f];
+                b2[f] = F.bmask[f];
+            }
+            gofs = g2;
+            bms = b2;
+        }
+    }
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
     __shared__ int kzc[kNCat];
@@ -312,10 +346,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     for (int f = tid; f < 2 * (SR + 8); f += nthr) xs[f] = F.consts[f];
     for (int f = tid; f < 3 * NB; f += nthr) kfs[f] = F.cls[f];
     for (int f = tid; f < 6 * NB; f += nthr) kgs[f] = F.kg[f];
-    for (int f = tid; f < 3 * NB * KS; f += nthr) {
-        gofs[f] = F.goff[f];
-        bms[f] = F.bmask[f];
-    }
     for (int f = tid; f < kNCat * SR * NP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
     if (tid < 3) cnt_sh[tid] = 0ull;
     if (wid == 0) { // TMEM (whole SM): the delta slots of every (group, block)
@@ -530,9 +560,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
                         if (ks < kf) far_step(ks, a, ad, bv, bw);
                         else loss_step(a, ad, bv, bw);
-                        const unsigned gmk = bms[vb * KS + ks];
+                        const unsigned gmk = F.lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
                         if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
-                            const double *gc = F.gcoef + static_cast<size_t>(gofs[vb * KS + ks]) * 32 + lane;
+                            const int go = F.lean ? __ldg(gofs + vb * KS + ks) : gofs[vb * KS + ks];
+                            const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
                             int rk = 0;
 #pragma unroll
                             for (int t = 0; t < TM; ++t) {
@@ -707,21 +738,26 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     }
 }
 
-/// Shared memory of a launch with NP points per batch.
-inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP) {
+/// Shared memory of a launch with NP points per batch; lean: carry rows and band tables
+/// in global memory.
+inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean) {
     const size_t MP = 2 * static_cast<size_t>(T.npairs);
-    return (static_cast<size_t>(kNCat) * T.SR * NP + static_cast<size_t>(kNCat) * T.nblk * NP + 2 * (T.SR + 8) + NP) *
-               sizeof(double) +
-           NP * 16 + NP * 8 + 9 * T.nblk * 4 + 3 * T.nblk * T.KS * 6 + MP * 4 + 4 * (MP + 1) * 4 +
-           2 * T.nblk * 4 + MP * T.nblk * 2 + 16;
+    size_t b = (static_cast<size_t>(kNCat) * T.SR * NP + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
+               9 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
+               MP * T.nblk * 2 + 16;
+    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double) + 3 * T.nblk * T.KS * 6;
+    return b;
 }
 
 template <int TM, int G, int MAXW>
 inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s, int nwarps) {
     constexpr int NP = G * 16;
-    const size_t smem = dmmag_smem_bytes(T, NP);
-    if (smem > 227 * 1024 || nwarps > MAXW) return -1;
+    const bool lean = dmmag_smem_bytes(T, NP, false) > 227 * 1024;
+    const size_t smem = dmmag_smem_bytes(T, NP, lean);
+    if (smem > 227 * 1024 || nwarps > MAXW || (lean && !T.carry_g)) return -1;
     DmmagArgs F{};
+    F.lean = lean;
+    F.carry_g = T.carry_g;
     F.KS = T.KS;
     F.nblk = T.nblk;
     F.SR = T.SR;
@@ -751,11 +787,12 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     return 0;
 }
 
-/// Point groups per batch: the most (<= 3) whose spectra fit in shared memory.
+/// Point groups per batch: the most (<= 3) whose spectra fit in shared memory (lean
+/// layout only for a single group).
 inline int dmmag_groups(const DmmagTables &T) {
     for (int G = 3; G >= 1; --G)
-        if (dmmag_smem_bytes(T, 16 * G) <= 227 * 1024) return G;
-    return 0;
+        if (dmmag_smem_bytes(T, 16 * G, false) <= 227 * 1024) return G;
+    return dmmag_smem_bytes(T, 16, true) <= 227 * 1024 ? 1 : 0;
 }
 
 /// Whether launch_dmmag takes this context's grid (same envelope, no launch).

@@ -20,7 +20,7 @@ def forced(monkeypatch):
     monkeypatch.setenv("FSBM_FAST_KERNEL", "dmmag")
 
 
-@pytest.mark.parametrize("nkr", [17, 66, 132])
+@pytest.mark.parametrize("nkr", [17, 66, 132, 264])
 def test_default_dispatch_picks_dmmag(nkr):
     ctx, _, _ = make_ctx(nkr)
     assert ctx.fast_kernel() == "coal_dmmag"
@@ -37,6 +37,8 @@ def test_default_dispatch_picks_dmmag(nkr):
     (90, None, "levels", (1, 3, 17)),  # 12 blocks: 16-point batches (shared-memory fit)
     (132, None, "levels", (1, 2, 19)), # 17 blocks, targets up to o+5
     (132, None, "random", (1, 2, 13)),
+    (264, None, "levels", (1, 1, 21)), # 33 blocks, targets up to o+9, lean shared-memory layout
+    (200, None, "random", (1, 1, 9)),
 ])
 def test_dmmag_vs_oracle(oracle, forced, nkr, ratio, pmode, dims):
     ctx, grid, tabs = make_ctx(nkr, ratio=ratio)
