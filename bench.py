@@ -215,10 +215,20 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def config_label(args):
+    """BASELINE.json configs: C2 (33 bins) is the headline; C3/C4 (66/132 bins) share its
+    grid; C5 (264 bins, 850x600x50 over 8 GPUs) is run as one GPU's patch."""
+    if (args.ni, args.nj, args.nk) == (425, 300, 50):
+        return {33: "C2", 66: "C3", 132: "C4"}.get(args.nkr, "C2-grid")
+    if args.nkr == 264 and (args.nj, args.nk) == (600, 50):
+        return "C5 per-GPU patch"
+    return "custom"
+
+
 def config_block(args, world):
     scale = getattr(args, "scaling", "weak")
     ni_g = args.ni * world if scale == "weak" else args.ni
-    return {"workload": f"C2 CONUS-12km {args.ni}x{args.nj}x{args.nk} (i x j x k) per GPU"
+    return {"workload": f"{config_label(args)} CONUS-12km {args.ni}x{args.nj}x{args.nk} (i x j x k) per GPU"
                         f"{' (weak: N stacked C2 slabs)' if scale == 'weak' and world > 1 else ''}, "
                         f"{args.nkr} bins, thunderstorm all-category input, cf {args.cf}, "
                         f"dt 1 s, 1 substep",
@@ -327,6 +337,7 @@ def run_ours(args):
             "frac": achieved / peak.value, "traffic": None,
             "peak_source": "measured live: fsbm_probe_fp64_peak DFMA-chain microbenchmark "
                            "(MEASURED_PEAKS.json has no FP64 entry)",
+            "kernel": ctx.fast_kernel() if args.numerics == "fast" else "coal_exact",
             "flop_per_update": FLOP_PER_TRIPLE * local_triples / max(1.0, cnt.points / args.steps),
             "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / step_ms,
             "hbm_bytes_per_update": 96 * nkr + 16}
