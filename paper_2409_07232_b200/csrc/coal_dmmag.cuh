@@ -552,37 +552,67 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         loadb(ks, bv, bw);
                         far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
                     }
-                    // (2) general steps: far or loss, plus the gather entries of the step
-                    for (; ks < min(kend, max(kf, kgh)); ++ks) {
-                        const double2 kk = __ldg(ga + ks * 32);
-                        double bv[NT], bw[NT];
-                        loadb(ks, bv, bw);
-                        const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
-                        if (ks < kf) far_step(ks, a, ad, bv, bw);
-                        else loss_step(a, ad, bv, bw);
-                        const unsigned gmk = F.lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
-                        if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
+                    // (2) general steps: far or loss, plus the gather entries of the step.  The
+                    // gather operands (weights, shifted A rows) are loaded first so their L2
+                    // latency overlaps the step's own DMMAs; the next A fragment is prefetched.
+                    {
+                        const int k2end = min(kend, max(kf, kgh));
+                        double2 kkn = ks < k2end ? __ldg(ga + ks * 32) : double2{0.0, 0.0};
+                        for (; ks < k2end; ++ks) {
+                            const double2 kk = kkn;
+                            if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
+                            const unsigned gmk = F.lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
                             const int go = F.lean ? __ldg(gofs + vb * KS + ks) : gofs[vb * KS + ks];
-                            const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
-                            int rk = 0;
+                            constexpr int TP = TM <= 6 ? TM : 1; // operands held ahead (registers)
+                            double cpre[TP];
+                            double2 kpre[TP];
+                            {
+                                const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
+                                int rk = 0;
 #pragma unroll
-                            for (int t = 0; t < TM; ++t) {
-                                if (gmk >> t & 1u) {
-                                    const double c = __ldg(gc + 32 * rk);
-                                    ++rk;
-                                    double at = a, adt = ad;
-                                    if (t > 0) {
-                                        const int ot = max(o - t, 0); // rows < 0 carry c == 0
-                                        const double2 k2 = __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
-                                                                 (((ot & 7) << 2) | lc));
-                                        at = uni ? fma(wu, k2.y, k2.x) : k2.x;
-                                        adt = k2.y;
-                                    }
-                                    const double a2 = at * c, ad2 = adt * c;
+                                for (int t = 0; t < TP; ++t) {
+                                    const bool ont = gmk >> t & 1u;
+                                    cpre[t] = ont ? __ldg(gc + 32 * rk) : 0.0;
+                                    rk += ont ? 1 : 0;
+                                    const int ot = max(o - t, 0); // rows < 0 carry c == 0
+                                    kpre[t] = ont && t > 0 ? __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
+                                                                   (((ot & 7) << 2) | lc))
+                                                           : double2{0.0, 0.0};
+                                }
+                            }
+                            double bv[NT], bw[NT];
+                            loadb(ks, bv, bw);
+                            const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
+                            if (ks < kf) far_step(ks, a, ad, bv, bw);
+                            else loss_step(a, ad, bv, bw);
+                            if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
+                                const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
+                                int rk = 0;
 #pragma unroll
-                                    for (int nt = 0; nt < NT; ++nt) {
-                                        dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
-                                        if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
+                                for (int t = 0; t < TM; ++t) {
+                                    if (gmk >> t & 1u) {
+                                        double c, at = a, adt = ad;
+                                        if (t < TP) {
+                                            c = cpre[t];
+                                            if (t > 0) {
+                                                at = uni ? fma(wu, kpre[t].y, kpre[t].x) : kpre[t].x;
+                                                adt = kpre[t].y;
+                                            }
+                                        } else {
+                                            c = __ldg(gc + 32 * rk);
+                                            const int ot = max(o - t, 0);
+                                            const double2 k2 = __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
+                                                                     (((ot & 7) << 2) | lc));
+                                            at = uni ? fma(wu, k2.y, k2.x) : k2.x;
+                                            adt = k2.y;
+                                        }
+                                        ++rk;
+                                        const double a2 = at * c, ad2 = adt * c;
+#pragma unroll
+                                        for (int nt = 0; nt < NT; ++nt) {
+                                            dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
+                                            if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
+                                        }
                                     }
                                 }
                             }
