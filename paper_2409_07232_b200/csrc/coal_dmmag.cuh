@@ -271,16 +271,16 @@ constexpr int kGSlotCols = 48; // TMEM columns of one (group, block) delta slot:
 /// Work unit = (pass, point group g, row block b), index i = b*G + g.  Unit i's deltas live
 /// in TMEM lane quadrant i % 4, slot i / 4: only that quadrant's warps can reach the slot,
 /// and they take the quadrant's units dynamically, in pass order, from one atomic counter.
-template <int TM, int G, int MAXW>
+template <int TM, int G, int MAXW, bool PAD>
 __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, DmmagArgs F) {
-    constexpr int NT = kGNT, NP = G * 16;
+    constexpr int NT = kGNT, NP = G * 16, QP = PAD ? NP + 4 : NP;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nkr = A.nkr, SR = F.SR, KS = F.KS, NB = F.nblk;
     const int npairs = A.pairs.npairs, MP = 2 * npairs; // passes per substep (upper bound)
     // shared-memory layout (dmmag_smem_bytes); the carry rows and the band tables move to
     // global memory when the spectra leave no room (F.lean: 264-bin grids)
-    double *work = reinterpret_cast<double *>(smem_raw);                     // [6][SR][NP]
-    double *xs = work + static_cast<size_t>(kNCat) * SR * NP;                // [SR+8]
+    double *work = reinterpret_cast<double *>(smem_raw);                     // [6][SR][QP]
+    double *xs = work + static_cast<size_t>(kNCat) * SR * QP;                // [SR+8]
     double *iw = xs + SR + 8;                                                 // [SR+8]
     double *wts = iw + SR + 8;                                                // [NP]
     unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP); // [NP]
@@ -334,10 +334,13 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     const double dt = A.dt_sub;
     const int nslots = (NB * G - 1) / 4 + 1; // slots per quadrant
 
-    // point-minor spectra, bit 3 of the point index swizzled by the bin's parity: the
-    // four K rows of a B fragment (8 points each) then hit disjoint bank halves
+    // point-minor spectra.  PAD: row pitch NP+4 doubles (= 4 mod 16), so the 4 K rows of a
+    // B fragment, the 8 owner rows of an emission and the 8 bins of a load each spread over
+    // all banks (2 wavefronts per 256 B, the minimum).  Otherwise (264-bin lean layout)
+    // bit 3 of the point index is swizzled by the bin's parity, which keeps the B fragments
+    // conflict free.
     auto W = [&](int c, int s, int q) -> double & {
-        return work[(static_cast<size_t>(c) * SR + s) * NP + (q ^ ((s & 1) << 3))];
+        return work[(static_cast<size_t>(c) * SR + s) * QP + (PAD ? q : (q ^ ((s & 1) << 3)))];
     };
     auto CR = [&](int c, int g, int b, int q) -> double & {
         return carry[((static_cast<size_t>(c) * G + g) * NB + b) * 16 + q];
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     for (int f = tid; f < 2 * (SR + 8); f += nthr) xs[f] = F.consts[f];
     for (int f = tid; f < 3 * NB; f += nthr) kfs[f] = F.cls[f];
     for (int f = tid; f < 6 * NB; f += nthr) kgs[f] = F.kg[f];
-    for (int f = tid; f < kNCat * SR * NP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
+    for (int f = tid; f < kNCat * SR * QP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
     if (tid < 3) cnt_sh[tid] = 0ull;
     if (wid == 0) { // TMEM (whole SM): the delta slots of every (group, block)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
@@ -770,20 +773,37 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 
 /// Shared memory of a launch with NP points per batch; lean: carry rows and band tables
 /// in global memory.
-inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean) {
+inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean, bool pad) {
     const size_t MP = 2 * static_cast<size_t>(T.npairs);
-    size_t b = (static_cast<size_t>(kNCat) * T.SR * NP + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
+    size_t b = (static_cast<size_t>(kNCat) * T.SR * (NP + (pad ? 4 : 0)) + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
                9 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
                MP * T.nblk * 2 + 16;
     if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double) + 3 * T.nblk * T.KS * 6;
     return b;
 }
 
-template <int TM, int G, int MAXW>
-inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s, int nwarps) {
+/// Launch geometry: point groups, padded rows, lean (global carry/band tables).
+struct DmmagGeom {
+    int G = 0;
+    bool pad = false, lean = false;
+};
+
+/// Most point groups (<= 3) that fit, padded rows preferred; the lean layout only for one group.
+inline DmmagGeom dmmag_geom(const DmmagTables &T) {
+    constexpr size_t kMax = 227 * 1024;
+    for (int G = 3; G >= 1; --G)
+        for (int pad = 1; pad >= 0; --pad)
+            if (dmmag_smem_bytes(T, 16 * G, false, pad) <= kMax) return DmmagGeom{G, pad != 0, false};
+    for (int pad = 1; pad >= 0; --pad)
+        if (dmmag_smem_bytes(T, 16, true, pad) <= kMax) return DmmagGeom{1, pad != 0, true};
+    return DmmagGeom{};
+}
+
+template <int TM, int G, int MAXW, bool PAD>
+inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s, int nwarps,
+                          bool lean) {
     constexpr int NP = G * 16;
-    const bool lean = dmmag_smem_bytes(T, NP, false) > 227 * 1024;
-    const size_t smem = dmmag_smem_bytes(T, NP, lean);
+    const size_t smem = dmmag_smem_bytes(T, NP, lean, PAD);
     if (smem > 227 * 1024 || nwarps > MAXW || (lean && !T.carry_g)) return -1;
     DmmagArgs F{};
     F.lean = lean;
@@ -801,7 +821,7 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     F.goff = T.goff;
     F.kg = T.kg;
     F.gcoef = T.gcoef;
-    auto kern = coal_dmmag_kernel<TM, G, MAXW>;
+    auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess) {
         fast_err() = "dmmag path: cannot reserve shared memory";
@@ -817,32 +837,31 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     return 0;
 }
 
-/// Point groups per batch: the most (<= 3) whose spectra fit in shared memory (lean
-/// layout only for a single group).
-inline int dmmag_groups(const DmmagTables &T) {
-    for (int G = 3; G >= 1; --G)
-        if (dmmag_smem_bytes(T, 16 * G, false) <= 227 * 1024) return G;
-    return dmmag_smem_bytes(T, 16, true) <= 227 * 1024 ? 1 : 0;
-}
-
 /// Whether launch_dmmag takes this context's grid (same envelope, no launch).
 inline bool dmmag_supported(const DmmagTables &T) {
-    const int G = dmmag_groups(T);
-    return T.stages && T.npairs <= kMaxPairs && G > 0 && (T.nblk * G - 1) / 4 + 1 <= 512 / kGSlotCols;
+    const DmmagGeom g = dmmag_geom(T);
+    return T.stages && T.npairs <= kMaxPairs && g.G > 0 && (T.nblk * g.G - 1) / 4 + 1 <= 512 / kGSlotCols;
 }
 
 /// Returns -1 when this geometry cannot run the general DMMA path.  Warps: 16 (128
 /// registers) for target offsets <= 4, else 12 (168 registers); FSBM_DMMAG_WARPS overrides.
 inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
     if (!T.stages || A.nkr != T.nkr || !dmmag_supported(T)) return -1;
-    const int G = dmmag_groups(T);
+    const DmmagGeom g = dmmag_geom(T);
     int nw = T.TM <= 4 ? 16 : 12;
     if (const char *ev = std::getenv("FSBM_DMMAG_WARPS")) nw = std::max(4, std::min(nw, std::atoi(ev)));
 #define FSBM_DG(TM_, MW_)                                                                          \
-    switch (G) {                                                                                   \
-    case 3: return launch_dmmag_t<TM_, 3, MW_>(T, A, num_sms, s, nw);                              \
-    case 2: return launch_dmmag_t<TM_, 2, MW_>(T, A, num_sms, s, nw);                              \
-    default: return launch_dmmag_t<TM_, 1, MW_>(T, A, num_sms, s, nw);                             \
+    if (g.pad) {                                                                                   \
+        switch (g.G) {                                                                             \
+        case 3: return launch_dmmag_t<TM_, 3, MW_, true>(T, A, num_sms, s, nw, g.lean);            \
+        case 2: return launch_dmmag_t<TM_, 2, MW_, true>(T, A, num_sms, s, nw, g.lean);            \
+        default: return launch_dmmag_t<TM_, 1, MW_, true>(T, A, num_sms, s, nw, g.lean);           \
+        }                                                                                          \
+    }                                                                                              \
+    switch (g.G) {                                                                                 \
+    case 3: return launch_dmmag_t<TM_, 3, MW_, false>(T, A, num_sms, s, nw, g.lean);               \
+    case 2: return launch_dmmag_t<TM_, 2, MW_, false>(T, A, num_sms, s, nw, g.lean);               \
+    default: return launch_dmmag_t<TM_, 1, MW_, false>(T, A, num_sms, s, nw, g.lean);              \
     }
     switch (T.TM) {
     case 2: FSBM_DG(2, 16)
