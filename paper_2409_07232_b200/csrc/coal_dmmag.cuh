@@ -80,7 +80,9 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
     if (nkr < 8 || nkr > 320) return 0;
     const int S = (nkr + 3) / 4 * 4, KS = S / 4, nblk = (nkr + 7) / 8, SR = nblk * 8;
     // far-cell weights are recomputed on the fly: c0 = (x[o+1] - (x[o] + x[s])) / width[o]
-    // (one multiply by the reciprocal; checked against the GainTable per far cell below)
+    // = 1 - x[s] / width[o], one FMA with the reciprocal width (checked against the
+    // GainTable per far cell below: within 1e-14 -- the reference's own x[o] + x[s]
+    // rounding is ~1e-15 of the weight at 132 bins -- or the cell leaves the far class)
     std::vector<double> xs(SR + 8), iw(SR + 8, 0.0);
     for (int k = 0; k < SR + 8; ++k) xs[k] = x[std::min(k, nkr - 1)];
     for (int k = 0; k + 1 < nkr; ++k) iw[k] = 1.0 / (x[k + 1] - x[k]);
@@ -116,9 +118,9 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                         const int o = 8 * b + r, s = 4 * kf + c;
                         if (o >= nkr || s >= nkr) continue; // A is zero there
                         const size_t e = static_cast<size_t>(o) * nkr + s;
-                        const double c0 = (xs[o + 1] - (xs[o] + xs[s])) * iw[o];
+                        const double c0 = fma(-xs[s], iw[o], 1.0); // == (x[o+1] - m) / width[o]
                         far = vmask(V, o, s) == 1.0 && s < o && g_lo[e] == o &&
-                              std::fabs(g_wlo[e] + g_whi[e] - 1.0) <= 4e-16 && std::fabs(c0 - g_wlo[e]) <= 4e-16;
+                              std::fabs(g_wlo[e] + g_whi[e] - 1.0) <= 4e-16 && std::fabs(c0 - g_wlo[e]) <= 1e-14;
                     }
                 if (!far) break;
             }
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     const int vb = V * NB + b;
                     const int kf = kfs[vb], kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
                     const int kend = min(KS, (kzs >> 2) + 1);
-                    const double xo = xs[o], xo1 = xs[o + 1], iwo = iw[o];
+                    const double iwo = iw[o];
                     const double2 *gi = F.stages + static_cast<size_t>(F.item_base[p] + X) * NB * KS * 32;
                     const double2 *ga = gi + static_cast<size_t>(b) * KS * 32 + lane;
                     // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         }
                     };
                     auto far_step = [&](int ks, double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
-                        const double c0 = (xo1 - (xo + xs[4 * ks + lc])) * iwo;
+                        const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
                         const double a2 = a * c0, ad2 = ad * c0;
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
