@@ -241,33 +241,6 @@ struct DmmagArgs {
     const double *gcoef;
 };
 
-// ---- TMEM as the delta store (tcgen05.ld/st, 32x32b shape: thread i <-> TMEM lane base+i) ----
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-/// tcgen05.ld without the wait: the registers are valid only after tm_wait_ld().
-__device__ __forceinline__ void tm_ld4_nowait(uint32_t taddr, double (&v)[4]) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr)
-                 : "memory");
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
-}
-__device__ __forceinline__ void tm_st4_nowait(uint32_t taddr, const double (&v)[4]) {
-    uint32_t r[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        r[2 * i] = static_cast<uint32_t>(__double2loint(v[i]));
-        r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v[i]));
-    }
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
 constexpr int kGSlotCols = 48; // TMEM columns of one (group, block) delta slot: 6 categories x 4 doubles
 
 /// Work unit = (pass, point group g, row block b), index i = b*G + g.  Unit i's deltas live
