@@ -472,13 +472,14 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
 #ifdef FSBM_DMMA_TMEM
     __shared__ uint32_t tmem_base;
     if (wid == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    const uint32_t tmw = tmem_base + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + (wid >> 2) * 48;
+    // this warp's slot: lanes 32*(wid%4).., columns (wid/4)*96: [0,48) deltas, [48,96) carries
+    const uint32_t tmw = tmem_base + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + (wid >> 2) * 96;
 #else
     __syncthreads();
 #endif
@@ -564,7 +565,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             {
                 const double z[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int c = 0; c < kNCat; ++c) tm_st4_nowait(tmw + 8 * c, z);
+                for (int c = 0; c < 2 * kNCat; ++c) tm_st4_nowait(tmw + 8 * c, z); // deltas, carries
                 tm_wait_st();
             }
 #else
@@ -737,6 +738,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     PROF_MARK(3)
                     // emission: rows o, points qg+nt*8+2lc+e; hi-gain -> row o+1
                     DmmaAcc L, Gn;
+#ifdef FSBM_DMMA_TMEM
+                    DmmaAcc Cy;
+#endif
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -747,15 +751,23 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             const double up = __shfl_up_sync(0xffffffffu, y3, 4);
                             L[nt][e] = f * Y1[nt][e];
                             Gn[nt][e] = lr > 0 ? fma(f, Y2[nt][e], up) : f * Y2[nt][e];
+#ifdef FSBM_DMMA_TMEM
+                            Cy[nt][e] = lr == 7 ? y3 : 0.0; // hi gain of row 7 -> next block head
+#else
                             if (lr == 7) carry[(static_cast<size_t>(pd) * RB + b) * NP + q] += y3;
+#endif
                         }
 #ifdef FSBM_DMMA_TMEM
                     {
-                        const uint32_t tf = tmw + 8 * fcat, tp = tmw + 8 * pd;
-                        double d[4], e4[4];
+                        const uint32_t tf = tmw + 8 * fcat, tp = tmw + 8 * pd, tcy = tmw + 48 + 8 * pd;
+                        double d[4], e4[4], cy[4];
                         tm_ld4_nowait(tf, d);
                         if (fcat != pd) tm_ld4_nowait(tp, e4);
+                        tm_ld4_nowait(tcy, cy);
                         tm_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) cy[i] += Cy[i >> 1][i & 1];
+                        tm_st4_nowait(tcy, cy);
                         if (fcat == pd) {
 #pragma unroll
                             for (int i = 0; i < 4; ++i) d[i] += Gn[i >> 1][i & 1] - L[i >> 1][i & 1];
@@ -912,6 +924,29 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 }
 #endif
             __syncthreads();
+#ifdef FSBM_DMMA_TMEM
+            // block-head carries from TMEM (lane row 7 holds them); the last block's go to
+            // the top row through tdel
+#pragma unroll
+            for (int c = 0; c < kNCat; ++c) {
+                double cy[4];
+                tm_ld4_nowait(tmw + 48 + 8 * c, cy);
+                tm_wait_ld();
+                if (lr == 7) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
+                        if (b + 1 < RB) W(c, 8 * (b + 1), q) = fma(dt, cy[i], W(c, 8 * (b + 1), q));
+                        else if (TAIL > 0) tdel[static_cast<size_t>(c) * NP + q] += cy[i];
+                    }
+                }
+            }
+            __syncthreads();
+            if (TAIL > 0)
+                for (int c = 0; c < kNCat; ++c)
+                    for (int q = tid; q < NP; q += nthr)
+                        W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q], W(c, ot, q));
+#else
             for (int c = 0; c < kNCat; ++c) // carries into block heads and the top row
                 for (int q = tid; q < NP; q += nthr) {
                     for (int bb = 1; bb < RB; ++bb)
@@ -921,6 +956,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                                                   carry[(static_cast<size_t>(c) * RB + RB - 1) * NP + q],
                                           W(c, ot, q));
                 }
+#endif
             __syncthreads();
             for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
                 for (int k = wid; k < nkr; k += NW)
@@ -967,7 +1003,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     __syncthreads();
     if (wid == 0) {
         tm_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 #endif
     for (int o = 16; o > 0; o >>= 1) {
