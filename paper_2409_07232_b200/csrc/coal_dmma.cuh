@@ -1060,23 +1060,24 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
     }
     const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
 #ifdef FSBM_DMMA_PROF
+    constexpr int kPW = kDmmaThreads / 32; // warps per CTA
     static unsigned long long *dprof = nullptr;
     if (!dprof) {
-        cudaMalloc(&dprof, 12 * 8 * 8);
-        cudaMemset(dprof, 0, 12 * 8 * 8);
+        cudaMalloc(&dprof, kPW * 8 * 8);
+        cudaMemset(dprof, 0, kPW * 8 * 8);
     }
     F.prof = dprof;
 #endif
     coal_dmma_kernel<<<grid, kDmmaThreads, smem, s>>>(A, F);
 #ifdef FSBM_DMMA_PROF
     {
-        unsigned long long h[96];
+        unsigned long long h[kPW * 8];
         cudaStreamSynchronize(s);
         cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost);
         static int calls = 0;
         if (++calls % 4 == 0) {
             fprintf(stderr, "dmma prof (Gcycles per warp, all CTAs): setup tail wait kloops barrier rest emit other\n");
-            for (int w = 0; w < 12; ++w) {
+            for (int w = 0; w < kPW; ++w) {
                 fprintf(stderr, "  w%2d b%d:", w, (w % 4 + w / 4) % 4);
                 for (int k = 0; k < 8; ++k) fprintf(stderr, " %7.2f", h[w * 8 + k] / 1e9);
                 fprintf(stderr, "\n");
