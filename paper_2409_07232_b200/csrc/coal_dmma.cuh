@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     // loops measured slower: the early exits break the schedule.)
     __shared__ int kzg[kDmmaG][kNCat];
     __shared__ int relcnt[kDmmaNBUF];
+    __shared__ short ltop[kNCat * kDmmaNP];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
     const int wid = tid >> 5, lane = tid & 31;
@@ -517,11 +518,16 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     const int k = kc + 8 * jj;
                     v[jj] = p != 0xffffffffu && k < nkr ? __ldg(src + k) : 0.0;
                 }
+                int top = -1; // last non-zero bin of this (category, point), for the first substep
 #pragma unroll
                 for (int jj = 0; jj < 5; ++jj) {
                     const int k = kc + 8 * jj;
                     if (k < S) W(c, k, q) = v[jj];
+                    if (v[jj] != 0.0) top = k;
                 }
+#pragma unroll
+                for (int d = 1; d < 8; d <<= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, d));
+                if (kc == 0) ltop[c * NP + q] = static_cast<short>(top);
             }
         }
         if (!gains_ready) {
@@ -537,9 +543,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             __syncthreads();
             for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
                 unsigned nz = 0;
-                for (int c = 0; c < kNCat; ++c) { // scanned from the top: last non-zero bin
-                    int l = nkr - 1;
-                    while (l >= 0 && W(c, l, q) == 0.0) --l;
+                for (int c = 0; c < kNCat; ++c) { // last non-zero bin (the load found it for sub 0)
+                    int l = ltop[c * NP + q];
+                    if (sub > 0) {
+                        l = nkr - 1;
+                        while (l >= 0 && W(c, l, q) == 0.0) --l;
+                    }
                     nz |= l >= 0 ? (1u << c) : 0u;
                     if (l >= 0 && pfail[q] == 0) atomicMax(&kzg[q / (NT * 8)][c], l);
                 }
