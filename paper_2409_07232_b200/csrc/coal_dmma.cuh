@@ -770,6 +770,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     {
                         const uint32_t tf = tmw + 8 * fcat, tp = tmw + 8 * pd, tcy = tmw + 48 + 8 * pd;
                         double d[4], e4[4], cy[4];
+                        tm_wait_st(); // the previous emission's stores (long complete by now)
                         tm_ld4_nowait(tf, d);
                         if (fcat != pd) tm_ld4_nowait(tp, e4);
                         tm_ld4_nowait(tcy, cy);
@@ -790,7 +791,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             tm_st4_nowait(tf, d);
                             tm_st4_nowait(tp, e4);
                         }
-                        tm_wait_st();
                     }
 #else
                     emit_switch(fcat * kNCat + pd, D, L, Gn);
@@ -856,6 +856,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
 #ifdef FSBM_DMMA_TMEM
                         if (__any_sync(0xffffffffu, e1 > e0)) {
                             double d[4];
+                            tm_wait_st();
                             tm_ld4_nowait(tmw + 8 * pd, d);
                             tm_wait_ld();
 #pragma unroll
@@ -910,6 +911,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             __syncthreads();
             PROF_MARK(4)
 #ifdef FSBM_DMMA_TMEM
+            tm_wait_st();
 #pragma unroll
             for (int c = 0; c < kNCat; ++c) {
                 double d[4];
