@@ -252,8 +252,15 @@ def run_ours(args):
     from paper_2409_07232_b200 import _lib, shard, synth
 
     world, rank, local = dist_env()
+    # FSBM_BENCH_ONE_GPU=1 (plumbing check only): every rank on cuda:0 over gloo, so the
+    # N>1 sharding / reduction path can be exercised on a one-GPU box; never a bench number
+    if os.environ.get("FSBM_BENCH_ONE_GPU") == "1":
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if os.environ.get("FSBM_BENCH_ONE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     lib = _lib.load()
