@@ -356,8 +356,8 @@ def run_ours(args):
     except Exception:
         pass
     try:  # DRAM bytes of the coal kernel from the committed ncu --set full capture, per launch
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
-        if tr["nkr"] == nkr:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))["by_nkr"].get(str(nkr))
+        if tr:
             roof["traffic"] = tr["bytes_per_update"] * (cnt.points / args.steps)
             roof["traffic_source"] = tr["source"]
     except Exception:
