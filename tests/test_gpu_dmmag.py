@@ -98,3 +98,22 @@ def test_dmmag_stiffness_first_point(oracle, forced):
     e = ei.value
     assert e.point == tuple(int(v) for v in err_o[2:5])
     assert (e.category, e.bin) == (int(err_o[0]), int(err_o[1]))
+
+
+@pytest.mark.parametrize("nkr", [33, 66])
+def test_dmmag_custom_registry_aliasing(oracle, forced, nkr):
+    """Non-standard registry through coal_dmmag: a==dest cross pair, 3-category pair,
+    repeated dest, a pair whose source_b is another pair's dest."""
+    pairs = [fsbm.InteractionPair("gl", 5, 0, 5), fsbm.InteractionPair("sl", 4, 0, 5),
+             fsbm.InteractionPair("ll", 0, 0, 0), fsbm.InteractionPair("il", 1, 0, 0),
+             fsbm.InteractionPair("sg", 4, 5, 5)]
+    ctx, grid, tabs = make_ctx(nkr, pairs=pairs, coeff=0.05)
+    assert ctx.fast_kernel() == "coal_dmmag"
+    st, mask, B = thunder_host(oracle, ctx, 2, 3, 7, 1.0, 9)
+    s, cnt_o, _, Bo = run_oracle_grid(oracle, ctx, tabs, st, mask, B, dt=0.2)
+    assert s == 0
+    cnt = fsbm.WorkCounters()
+    fsbm.fissioned_step(st, None, fsbm.StepContext(ctx, fsbm.CoalConfig(0.2), cnt), fsbm.ExecPlan())
+    got = np.stack([b.reshape(-1, nkr) for b in st.bins])
+    assert_close(got, Bo, f"dmmag custom registry nkr{nkr}")
+    assert [cnt.triples, cnt.points, cnt.kernel_evals] == [int(v) for v in cnt_o]
