@@ -37,6 +37,7 @@
 #include <cmath>
 #include <cstdint>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "coal_dmma.cuh"
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             allu = allu && wts[q] == wu;
                         }
                     }
-                    const bool uni = __all_sync(0xffffffffu, allu);
+                    const bool uni_rt = __all_sync(0xffffffffu, allu);
                     const int vb = V * NB + b;
                     const int kf = kfs[vb], kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
                     const int kend = min(KS, (kzs >> 2) + 1);
@@ -494,6 +495,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 #pragma unroll
                             for (int t = 0; t < TM; ++t) Z[t][nt][e] = 0.0;
                         }
+                    // the K-loops, compiled twice: one pressure weight for the whole group
+                    // (uni, the common case) or per-point weights (a group straddling a level)
+                    auto kloop = [&](auto UC) {
+                        constexpr bool uni = decltype(UC)::value;
                     auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
@@ -604,6 +609,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         loadb(ks, bv, bw);
                         loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
                     }
+                    };
+                    if (uni_rt) kloop(std::true_type{});
+                    else kloop(std::false_type{});
                     // owner emission values (dt at the apply); far-cell hi gains of row 7
                     // carry into the next block's head row
 #pragma unroll
