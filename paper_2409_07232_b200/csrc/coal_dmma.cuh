@@ -308,7 +308,8 @@ constexpr int kDmmaG = 4;
 constexpr int kDmmaG = 3;                           // point groups per CTA
 #endif
 constexpr int kDmmaNP = kDmmaG * kDmmaNT * 8;       // 48 points per batch
-constexpr int kDmmaThreads = kDmmaG * kDmmaRB * 32; // 384
+constexpr int kDmmaThreads = kDmmaG * kDmmaRB * 32; // 512 (TMEM) / 384
+constexpr int kDmmaQP = (kDmmaNP + 15) / 16 * 16 + 4; // point pitch, = 4 mod 16: conflict-free B fragments
 
 /// register delta add with a runtime (warp-uniform) category
 __device__ __forceinline__ void dadd_cat(double (&D)[kNCat][kDmmaNT][2], int cat, int nt, int e,
@@ -416,7 +417,8 @@ __device__ __forceinline__ void emit_switch(int sel, double (&D)[kNCat][kDmmaNT]
 __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, DmmaArgs F) {
     constexpr int NT = kDmmaNT, NP = kDmmaNP, RB = kDmmaRB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nkr = A.nkr, S = F.S, QP = F.QP, TAIL = F.tail;
+    const int nkr = A.nkr, S = F.S, TAIL = F.tail;
+    constexpr int QP = kDmmaQP; // compile-time: immediate offsets for the B-fragment loads
     const int KS = S / 4;
     const size_t TBL = static_cast<size_t>(S) * S;
     constexpr int NBUF = kDmmaNBUF;
@@ -1041,7 +1043,7 @@ inline size_t dmma_smem_bytes(int nkr, int S, int QP) {
 inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const StepArgs &A,
                        int num_sms, cudaStream_t s) {
     if (!T.blob || A.nkr != T.nkr) return -1;
-    const int QP = (kDmmaNP + 15) / 16 * 16 + 4; // = 4 mod 16: conflict-free B fragments
+    const int QP = kDmmaQP;
     const size_t smem = dmma_smem_bytes(A.nkr, T.S, QP);
     if (smem > 227 * 1024) return -1;
     DmmaArgs F{};
