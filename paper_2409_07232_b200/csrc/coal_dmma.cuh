@@ -328,10 +328,10 @@ __device__ __forceinline__ void dadd_cat(double (&D)[kNCat][kDmmaNT][2], int cat
 /// (full: ks < KF, diagonal: KF <= ks < KM, no owned gains: ks >= KM; KSN steps),
 /// fully unrolled so the A-fragment loads/interpolation are scheduled ahead of the
 /// DMMA chains.  INTERP: A = K500 + wu*Kd, else A = K500.
-template <int KF, int KM, int KSN, bool INTERP>
+template <int KF, int KM, int KSN, bool INTERP, int ASTRIDE>
 __device__ __forceinline__ void dmma_pass_single(const double *__restrict__ T5, const double *__restrict__ Td,
                                                  double wu, const double *__restrict__ Glo,
-                                                 const double *__restrict__ Ghi, int abase, int astride,
+                                                 const double *__restrict__ Ghi, int abase, int /*astride*/,
                                                  const double *__restrict__ vb, int QP, int V, int o, int lc,
                                                  double (&c1)[kDmmaNT][2], double (&c2)[kDmmaNT][2],
                                                  double (&cg)[kDmmaNT][2]) {
@@ -340,7 +340,7 @@ __device__ __forceinline__ void dmma_pass_single(const double *__restrict__ T5, 
     for (int nt = 0; nt < kDmmaNT; ++nt) cf[nt][0] = cf[nt][1] = c2[nt][0] = c2[nt][1] = cg[nt][0] = cg[nt][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < KSN; ++ks) {
-        const int ai = abase + ks * astride;
+        const int ai = abase + ks * ASTRIDE; // compile-time stride: immediate table offsets
         const double t = INTERP ? fma(wu, Td[ai], T5[ai]) : T5[ai];
         if (ks < KF) { // every cell owned-far: Y3 = YG - Y2 shares the loss DMMAs
             const double t2 = t * Glo[ai];
@@ -666,7 +666,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     if (unrolled) { // fully unrolled K-loops (the common case)
                         double c1[NT][2] = {}, c2[NT][2], cg[NT][2];
 #define FSBM_PASS(BB, IN)                                                                          \
-    dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg)
+    (X == 0 ? dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN, 4>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg) \
+            : dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN, 4 * 36>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg))
                         // one instantiation per block (K500 + w*Kd with w = 0 for p <= 500 hPa):
                         // halving the unrolled code keeps the kernel inside the instruction cache
                         const double wi = wmode == 1 ? wu : 0.0;
