@@ -247,11 +247,13 @@ constexpr int kGSlotCols = 48; // TMEM columns of one (group, block) delta slot:
 /// Work unit = (pass, point group g, row block b), index i = b*G + g.  Unit i's deltas live
 /// in TMEM lane quadrant i % 4, slot i / 4: only that quadrant's warps can reach the slot,
 /// and they take the quadrant's units dynamically, in pass order, from one atomic counter.
-template <int TM, int G, int MAXW, bool PAD>
+template <int TM, int G, int MAXW, bool PAD, int NKRC>
 __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, DmmagArgs F) {
     constexpr int NT = kGNT, NP = G * 16, QP = PAD ? NP + 4 : NP;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nkr = A.nkr, SR = F.SR, KS = F.KS, NB = F.nblk;
+    // NKRC != 0: a grid compiled in (66/132/264 bins) -- extents become immediates
+    const int nkr = NKRC ? NKRC : A.nkr, SR = NKRC ? 8 * ((NKRC + 7) / 8) : F.SR;
+    const int KS = NKRC ? (NKRC + 3) / 4 : F.KS, NB = NKRC ? (NKRC + 7) / 8 : F.nblk;
     const int npairs = A.pairs.npairs, MP = 2 * npairs; // passes per substep (upper bound)
     // shared-memory layout (dmmag_smem_bytes); the carry rows and the band tables move to
     // global memory when the spectra leave no room (F.lean: 264-bin grids)
@@ -782,7 +784,7 @@ inline DmmagGeom dmmag_geom(const DmmagTables &T) {
     return DmmagGeom{};
 }
 
-template <int TM, int G, int MAXW, bool PAD>
+template <int TM, int G, int MAXW, bool PAD, int NKRC = 0>
 inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s, int nwarps,
                           bool lean) {
     constexpr int NP = G * 16;
@@ -804,7 +806,8 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     F.goff = T.goff;
     F.kg = T.kg;
     F.gcoef = T.gcoef;
-    auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD>;
+    if (NKRC && NKRC != T.nkr) return -1;
+    auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD, NKRC>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess) {
         fast_err() = "dmmag path: cannot reserve shared memory";
@@ -833,6 +836,15 @@ inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cu
     const DmmagGeom g = dmmag_geom(T);
     int nw = T.TM <= 4 ? 16 : 12;
     if (const char *ev = std::getenv("FSBM_DMMAG_WARPS")) nw = std::max(4, std::min(nw, std::atoi(ev)));
+    // the BASELINE grids with their extents compiled in (FSBM_DMMAG_GENERIC=1: A/B)
+    if (!std::getenv("FSBM_DMMAG_GENERIC")) {
+        if (T.nkr == 66 && T.TM == 4 && g.G == 3 && g.pad && !g.lean)
+            return launch_dmmag_t<4, 3, 16, true, 66>(T, A, num_sms, s, nw, false);
+        if (T.nkr == 132 && T.TM == 6 && g.G == 1 && g.pad && !g.lean)
+            return launch_dmmag_t<6, 1, 12, true, 132>(T, A, num_sms, s, nw, false);
+        if (T.nkr == 264 && T.TM == 10 && g.G == 1 && !g.pad && g.lean)
+            return launch_dmmag_t<10, 1, 12, false, 264>(T, A, num_sms, s, nw, true);
+    }
 #define FSBM_DG(TM_, MW_)                                                                          \
     if (g.pad) {                                                                                   \
         switch (g.G) {                                                                             \
