@@ -414,10 +414,12 @@ __device__ __forceinline__ void emit_switch(int sel, double (&D)[kNCat][kDmmaNT]
 #undef FSBM_EMIT_CASE
 }
 
+template <int NKRC>
 __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, DmmaArgs F) {
     constexpr int NT = kDmmaNT, NP = kDmmaNP, RB = kDmmaRB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nkr = A.nkr, S = F.S, TAIL = F.tail;
+    // NKRC == 33: the headline grid with its extents compiled in (S = 36, one tail row)
+    const int nkr = NKRC ? NKRC : A.nkr, S = NKRC ? (NKRC + 3) / 4 * 4 : F.S, TAIL = NKRC ? NKRC % 8 : F.tail;
     constexpr int QP = kDmmaQP; // compile-time: immediate offsets for the B-fragment loads
     const int KS = S / 4;
     const size_t TBL = static_cast<size_t>(S) * S;
@@ -1067,7 +1069,9 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
     F.exc_off = T.exc_off;
     F.exc = T.exc;
     F.nexc = T.nexc;
-    if (cudaFuncSetAttribute(coal_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const bool c33 = A.nkr == 33 && F.std_classes && !std::getenv("FSBM_DMMA_GENERIC");
+    auto kern = c33 ? coal_dmma_kernel<33> : coal_dmma_kernel<0>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem)) != cudaSuccess) {
         fast_err() = "dmma path: cannot reserve shared memory";
         return 6;
@@ -1082,7 +1086,7 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
     }
     F.prof = dprof;
 #endif
-    coal_dmma_kernel<<<grid, kDmmaThreads, smem, s>>>(A, F);
+    kern<<<grid, kDmmaThreads, smem, s>>>(A, F);
 #ifdef FSBM_DMMA_PROF
     {
         unsigned long long h[kPW * 8];
