@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     // NKRC != 0: a grid compiled in (66/132/264 bins) -- extents become immediates
     const int nkr = NKRC ? NKRC : A.nkr, SR = NKRC ? 8 * ((NKRC + 7) / 8) : F.SR;
     const int KS = NKRC ? (NKRC + 3) / 4 : F.KS, NB = NKRC ? (NKRC + 7) / 8 : F.nblk;
+    const bool lean = NKRC ? NKRC == 264 : F.lean != 0; // compiled-in grids: layout known
     const int npairs = A.pairs.npairs, MP = 2 * npairs; // passes per substep (upper bound)
     // shared-memory layout (dmmag_smem_bytes); the carry rows and the band tables move to
     // global memory when the spectra leave no room (F.lean: 264-bin grids)
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     {
         unsigned char *tail = reinterpret_cast<unsigned char *>(rnk + MP * NB);
         tail += (16 - reinterpret_cast<uintptr_t>(tail) % 16) % 16;
-        if (F.lean) {
+        if (lean) {
             carry = F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP;
             gofs = F.goff;
             bms = F.bmask;
@@ -546,8 +547,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         for (; ks < k2end; ++ks) {
                             const double2 kk = kkn;
                             if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
-                            const unsigned gmk = F.lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
-                            const int go = F.lean ? __ldg(gofs + vb * KS + ks) : gofs[vb * KS + ks];
+                            const unsigned gmk = lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
+                            const int go = lean ? __ldg(gofs + vb * KS + ks) : gofs[vb * KS + ks];
                             constexpr int TP = TM <= 6 ? TM : 1; // operands held ahead (registers)
                             double cpre[TP];
                             double2 kpre[TP];
