@@ -544,7 +544,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     {
                         const int k2end = min(kend, max(kf, kgh));
                         double2 kkn = ks < k2end ? __ldg(ga + ks * 32) : double2{0.0, 0.0};
-                        for (; ks < k2end; ++ks) {
+                        // one copy of the step for far K-steps, one for the others: no per-step branch
+                        auto step2 = [&](int ks, auto FC) {
+                            constexpr bool FAR = decltype(FC)::value;
                             const double2 kk = kkn;
                             if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
                             const unsigned gmk = lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
@@ -569,7 +571,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             double bv[NT], bw[NT];
                             loadb(ks, bv, bw);
                             const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
-                            if (ks < kf) far_step(ks, a, ad, bv, bw);
+                            if constexpr (FAR) far_step(ks, a, ad, bv, bw);
                             else loss_step(a, ad, bv, bw);
                             if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
                                 const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
@@ -602,7 +604,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                     }
                                 }
                             }
-                        }
+                        };
+                        for (; ks < min(k2end, kf); ++ks) step2(ks, std::true_type{});
+                        for (; ks < k2end; ++ks) step2(ks, std::false_type{});
                     }
                     // (3) loss-only steps above the band
 #pragma unroll 4
