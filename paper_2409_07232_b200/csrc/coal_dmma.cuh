@@ -25,13 +25,17 @@
 // the loss DMMAs, so only the diagonal ("mixed") steps need a third product.
 //
 // Work split: warp (g, b) owns rows [8b, 8b+8) for the 16 points of group g over all
-// pairs, keeps its deltas in registers (deterministic, no atomics) and carries the
-// hi-gain of row 8b+7 to the next block through smem.  The 33rd (top) row is a
-// 4-row DMMA tile {P1, P2} x {500, d} done by the group's block-0 warp.  Per-pair
-// tables (T500, Kd: one [S][S] layout read row-wise by the row pass and transposed
-// by the column pass, both bank-conflict free at pitch S = 36) are double-buffered
-// in smem by 1-D TMA bulk copies; the last warp to release a buffer refills it with
-// the pair two ahead, so warps drift freely across pairs.
+// pairs (4 groups x 4 blocks = 16 warps, 64 points per batch).  Its deltas and the hi-gain
+// carry of row 8b+7 into the next block live in TMEM (tcgen05.alloc; one 96-column slot
+// per warp in its lane quadrant: deterministic, no atomics), which frees the registers
+// for 16 warps x 128 (-DFSBM_DMMA_NO_TMEM: the register/shared-memory variant, 12 warps).
+// The 33rd (top) row -- 1/8 of a DMMA tile -- is a scalar FP64 dot product split over
+// the group's four warps.  Per-pair tables (T500, Kd: one [S][S] layout read row-wise by
+// the row pass and transposed by the column pass, both bank-conflict free at pitch
+// S = 36) are triple-buffered in smem by 1-D TMA bulk copies; the last warp to release a
+// buffer refills it with the pair three ahead, so warps drift freely across pairs.  The
+// 33-bin grid is compiled in (nkr, pitch, tail row as immediates) and the unrolled
+// K-loops are specialised per block and pass direction.
 #pragma once
 
 #include <algorithm>
