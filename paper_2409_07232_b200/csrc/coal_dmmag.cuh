@@ -1,36 +1,29 @@
-// coal_dmmag.cuh -- FSBM_NUMERICS_FAST on the FP64 tensor cores (DMMA.8x8x4) for any bin
-// count whose flux targets stay within 9 bins of the owner (66 and 132 bins on the
-// equal-range grids of SURVEY 8(d); the tuned 32/33-bin kernel is coal_dmma.cuh).
+// coal_dmmag.cuh -- FSBM_NUMERICS_FAST on the FP64 tensor cores (DMMA.8x8x4) for grids
+// whose flux targets stay within nine bins of the owner: 66/132/264 bins on the
+// equal-range grids of SURVEY 8(d), and others (the tuned 32/33-bin kernel is coal_dmma.cuh).
 //
 // Same owner decomposition as coal_dmma.cuh / coal_fast.cuh (coalescence.cpp:204-339
 // reassociated): for a pair (a, b -> d) the row pass (owner o = i, stream s = j,
 // v = nb, f = na, loss -> a) and the column pass (o = j, s = i, v = na, f = nb,
 // loss -> b) compute per 8-row owner block and 8-point tile the GEMMs
-//     L[o,q]   = sum_s A(o,s) v_q[s]                 loss of bin o
-//     Z_t[o,q] = sum_s A(o,s) c_t(o,s) v_q[s]        gain into bin o+t, t = 0..TM-1
-// where c_t is the GainTable weight (coalescence.cpp:36-67) of cell (o,s) towards bin
-// o+t, restricted to the cells the owner owns (s < o; column pass and self-pair
-// diagonal s <= o, the latter halved, coalescence.cpp:293).  At 66/132 bins the
-// targets of a cell reach o+3 / o+5 (SURVEY 8(a) "band structure"), so unlike the
-// 33-bin kernel every offset has its own accumulator; the gain of row o+t lands in
-// the warp's own block or, past row 7, in a register "carry" block that is added to
-// the next block's rows at the Jacobi apply.
+//     L[o,q]   = sum_s A(o,s) v_q[s]                       loss of bin o
+//     Z_t[o,q] = sum_s A(o-t,s) c_t(o-t,s) v_q[s]          gain of owner row o-t into bin o
+// where c_t is the GainTable weight (coalescence.cpp:36-67) of a cell towards the bin t
+// above its owner (cells the owner owns: s < o; column pass and self-pair diagonal
+// s <= o, the latter halved, coalescence.cpp:293).  The gains are written in this
+// target-aligned "gather" form (A rows shifted by t, weights pre-arranged on the host as
+// fragments), so no multi-row carries exist.  "Far" K-steps (every cell targets {o, o+1}
+// with weights summing to 1) run two DMMAs -- X = sum A v, Y = sum A c0 v with
+// c0 = 1 - x_s / width_o -- and give the hi gain X - Y, carried one row (smem).
 //
-// K-step classes per (view, block): "far" steps (every cell targets {o, o+1} with
-// weights summing to 1) run two DMMAs -- X = sum A v and Y = sum A c0 v, with
-// Z_1 += X - Y --, "band" steps run the loss plus one DMMA per target offset present
-// in the tile, "upper" steps only the loss.  The weights are recomputed on the fly from
-// the mass grid (m = x_o + x_s, lo = o + delta(o - s), w = (x[lo+1] - m) / width) --
-// host-verified against the GainTable for every cell when the context is built --
-// so no pair-independent coefficient table occupies shared memory.
-//
-// Data movement: the per-pair kernel tables (K500, K750-K500) are pre-arranged on the
-// host in DMMA A-fragment order, chunked by K-steps ([pass][chunk][block][k][lane]),
-// and streamed into a 3-deep shared-memory ring by 1-D TMA bulk copies; the last warp
-// to release a buffer refills it.  The CTA's point spectra (all six categories) sit in
-// shared memory, point-minor and XOR-swizzled so B-fragment loads are conflict free.
-// A group whose 16 points share one pressure weight interpolates A in registers; a
-// group that straddles a level runs K500 against v and K750-K500 against w_q v.
+// Execution: the per-pass tables (K500, K750-K500) are pre-arranged in DMMA A-fragment
+// order ([pass][block][k][lane]) and streamed per warp from L2 by 512-byte loads; work
+// units (pass, point group, row block) are taken dynamically by the warps of the TMEM
+// lane quadrant that holds the unit's deltas (tcgen05.ld/st), in pass order, with a
+// per-block ticket that fixes the accumulation order (bitwise determinism).  Zero owner
+// rows and zero stream tails (the reference's rate == 0 skip) drop whole units and K-steps.
+// The K-loops are compiled twice (group-uniform vs per-point pressure weights) and the
+// band step twice (far / non-far); 66/132/264 bins are compiled in.
 #pragma once
 
 #include <algorithm>
