@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     for (int nt = 0; nt < NT; ++nt)
                         Y1[nt][0] = Y1[nt][1] = Y2[nt][0] = Y2[nt][1] = YG[nt][0] = YG[nt][1] = 0.0;
                     const int nhalf = wmode == 2 ? 2 : 1;
-                    const bool unrolled = F.std_classes && wmode != 2;
+                    const bool unrolled = (NKRC || F.std_classes) && wmode != 2;
                     if (unrolled) { // fully unrolled K-loops (the common case)
                         double c1[NT][2] = {}, c2[NT][2], cg[NT][2];
 #define FSBM_PASS(BB, IN)                                                                          \
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 }
                 PROF_MARK(1)
                 // exception cells (non owner-local targets), gathered by the target's owner
-                if (F.nexc > 0) {
+                if (!NKRC && F.nexc > 0) { // (the compiled-in 33-bin grid has none)
                     for (int kind = self ? 1 : 0; kind <= (self ? 1 : 2); kind += self ? 1 : 2) {
 #ifdef FSBM_DMMA_TMEM
                         double exd[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1073,7 +1073,7 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
     F.exc_off = T.exc_off;
     F.exc = T.exc;
     F.nexc = T.nexc;
-    const bool c33 = A.nkr == 33 && F.std_classes && !std::getenv("FSBM_DMMA_GENERIC");
+    const bool c33 = A.nkr == 33 && F.std_classes && T.nexc == 0 && !std::getenv("FSBM_DMMA_GENERIC");
     auto kern = c33 ? coal_dmma_kernel<33> : coal_dmma_kernel<0>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem)) != cudaSuccess) {
