@@ -383,6 +383,68 @@ __device__ __forceinline__ void dmma_pass_single(const double *__restrict__ T5, 
         }
 }
 
+/// The same pass for a group that straddles a pressure level: A = K500 + w_q Kd with a
+/// per-point weight, run as K500 . v + Kd . (w_q v) -- two DMMAs into the same
+/// accumulator, the lane's B column scaled by its point's weight wq[nt].
+template <int KF, int KM, int KSN, int ASTRIDE>
+__device__ __forceinline__ void dmma_pass_dual(const double *__restrict__ T5, const double *__restrict__ Td,
+                                               const double (&wq)[kDmmaNT], const double *__restrict__ Glo,
+                                               const double *__restrict__ Ghi, int abase,
+                                               const double *__restrict__ vb, int QP, int V, int o, int lc,
+                                               double (&c1)[kDmmaNT][2], double (&c2)[kDmmaNT][2],
+                                               double (&cg)[kDmmaNT][2]) {
+    double cf[kDmmaNT][2];
+#pragma unroll
+    for (int nt = 0; nt < kDmmaNT; ++nt) cf[nt][0] = cf[nt][1] = c2[nt][0] = c2[nt][1] = cg[nt][0] = cg[nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KSN; ++ks) {
+        const int ai = abase + ks * ASTRIDE;
+        const double t5 = T5[ai], td = Td[ai];
+        double v[kDmmaNT], vw[kDmmaNT];
+#pragma unroll
+        for (int nt = 0; nt < kDmmaNT; ++nt) {
+            v[nt] = vb[(4 * ks) * QP + nt * 8];
+            vw[nt] = wq[nt] * v[nt];
+        }
+        if (ks < KF) {
+            const double g = Glo[ai];
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                dmma(cf[nt][0], cf[nt][1], t5, v[nt]);
+                dmma(cf[nt][0], cf[nt][1], td, vw[nt]);
+                dmma(c2[nt][0], c2[nt][1], t5 * g, v[nt]);
+                dmma(c2[nt][0], c2[nt][1], td * g, vw[nt]);
+            }
+        } else if (ks < KM) {
+            const int s = 4 * ks + lc;
+            const double msk = V == 2 ? (s <= o ? 1.0 : 0.0) : (s < o ? 1.0 : (V == 1 && s == o ? 0.5 : 0.0));
+            const double lo = msk * Glo[ai], hi = msk * Ghi[ai];
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                dmma(c1[nt][0], c1[nt][1], t5, v[nt]);
+                dmma(c1[nt][0], c1[nt][1], td, vw[nt]);
+                dmma(c2[nt][0], c2[nt][1], t5 * lo, v[nt]);
+                dmma(c2[nt][0], c2[nt][1], td * lo, vw[nt]);
+                dmma(cg[nt][0], cg[nt][1], t5 * (lo + hi), v[nt]);
+                dmma(cg[nt][0], cg[nt][1], td * (lo + hi), vw[nt]);
+            }
+        } else {
+#pragma unroll
+            for (int nt = 0; nt < kDmmaNT; ++nt) {
+                dmma(c1[nt][0], c1[nt][1], t5, v[nt]);
+                dmma(c1[nt][0], c1[nt][1], td, vw[nt]);
+            }
+        }
+    }
+#pragma unroll
+    for (int nt = 0; nt < kDmmaNT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            c1[nt][e] += cf[nt][e];
+            cg[nt][e] += cf[nt][e];
+        }
+}
+
 typedef double DmmaAcc[kDmmaNT][2];
 
 /// D[FC] -= L, D[PD] += G with compile-time categories: one indirect branch per pass
@@ -668,9 +730,25 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     for (int nt = 0; nt < NT; ++nt)
                         Y1[nt][0] = Y1[nt][1] = Y2[nt][0] = Y2[nt][1] = YG[nt][0] = YG[nt][1] = 0.0;
                     const int nhalf = wmode == 2 ? 2 : 1;
-                    const bool unrolled = (NKRC || F.std_classes) && wmode != 2;
+                    // compiled-in grid: a level-straddling group runs the unrolled dual pass
+                    const bool unrolled = NKRC ? true : (F.std_classes && wmode != 2);
                     if (unrolled) { // fully unrolled K-loops (the common case)
                         double c1[NT][2] = {}, c2[NT][2], cg[NT][2];
+                        if (NKRC && wmode == 2) {
+                            double wqq[NT];
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) wqq[nt] = wts[qg + 8 * nt + lr];
+#define FSBM_PASS2(BB)                                                                             \
+    (X == 0 ? dmma_pass_dual<2 * BB, 2 * BB + 2, 9, 4>(T5, Td, wqq, Glo, Ghi, abase, vb, QP, V, o, lc, c1, c2, cg) \
+            : dmma_pass_dual<2 * BB, 2 * BB + 2, 9, 4 * 36>(T5, Td, wqq, Glo, Ghi, abase, vb, QP, V, o, lc, c1, c2, cg))
+                            switch (b) {
+                            case 0: FSBM_PASS2(0); break;
+                            case 1: FSBM_PASS2(1); break;
+                            case 2: FSBM_PASS2(2); break;
+                            default: FSBM_PASS2(3); break;
+                            }
+#undef FSBM_PASS2
+                        } else {
 #define FSBM_PASS(BB, IN)                                                                          \
     (X == 0 ? dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN, 4>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg) \
             : dmma_pass_single<2 * BB, 2 * BB + 2, 9, IN, 4 * 36>(T5, Td, wi, Glo, Ghi, abase, astride, vb, QP, V, o, lc, c1, c2, cg))
@@ -684,6 +762,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         default: FSBM_PASS(3, true); break;
                         }
 #undef FSBM_PASS
+                        }
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
