@@ -22,7 +22,7 @@ extern "C" {
 #endif
 
 #define FSBM_NCAT 6
-#define FSBM_ABI_VERSION 1
+#define FSBM_ABI_VERSION 2
 
 /* Error taxonomy of errors.hpp:10-74 as status codes. */
 typedef enum {
@@ -76,11 +76,13 @@ typedef struct {
     uint64_t kernel_evals;
 } fsbm_counters;
 
-/* StiffnessError (errors.hpp:35-62) incl. at_point (1-based i,k,j). */
+/* StiffnessError (errors.hpp:35-62) incl. at_point (1-based i,k,j) and the negative
+ * value the reference prints in its message (coalescence.cpp:319-325). */
 typedef struct {
     int category, bin;
     int has_point;
     int i, k, j;
+    double value;
 } fsbm_error;
 
 typedef struct fsbm_ctx fsbm_ctx; /* opaque: device tables, gain table, registry */
@@ -133,6 +135,23 @@ int fsbm_step_grid_host(fsbm_ctx *ctx, fsbm_ranges ranges, double *const bins_h[
                         const uint8_t *mask_h, double dt, int substeps, const fsbm_plan *plan,
                         const fsbm_tile *tiles, int ntiles, fsbm_counters *counters_out,
                         fsbm_error *err_out);
+
+/* fsbm_step_grid_host on the patch `patch` (global 1-based extents, an i/j sub-range with
+ * all of k) of a host GridState whose arrays span `global`: the caller passes the GLOBAL
+ * arrays, the H2D/D2H copies are pitched (one (i,k) line of the patch per row), so a
+ * WRF-style j-patch (decompose, driver.cpp:187-196) is stepped in place without a
+ * host-side gather.  fsbm_step_grid_host(r) == fsbm_step_patch_host(r, r). */
+int fsbm_step_patch_host(fsbm_ctx *ctx, fsbm_ranges global, fsbm_ranges patch,
+                         double *const bins_h[FSBM_NCAT], const double *pressure_h,
+                         const double *temperature_h, const uint8_t *mask_h, double dt,
+                         int substeps, const fsbm_plan *plan, const fsbm_tile *tiles, int ntiles,
+                         fsbm_counters *counters_out, fsbm_error *err_out);
+
+/* Diagnostics of a device state: out[c] = sum of n over all points and bins of category c,
+ * out[6 + c] = sum of n*x[bin] (total_number / total_mass, mass_grid.hpp, summed over the
+ * grid; deterministic order for a given npoints).  Synchronises `stream`. */
+int fsbm_state_moments_device(fsbm_ctx *ctx, size_t npoints, const double *const bins_d[FSBM_NCAT],
+                              double out[2 * FSBM_NCAT], void *stream);
 
 /* coal_step (coalescence.hpp:148-150) for ONE point on host spans (bins6 is
  * category-major [6][nkr]); a one-point launch.  Error semantics as coal_step
@@ -213,6 +232,77 @@ int fsbm_compare_states_device(int device, size_t npoints, int nkr, const double
                                const double *temperature_b, const double *pressure_b,
                                const double *const bins_b[FSBM_NCAT], fsbm_field_diff *out,
                                void *stream);
+
+/* ---- multi-GPU: shards, device groups, NCCL diagnostics ----
+ *
+ * Microphysics is column-local: shards are independent, there is no halo and no
+ * data-path collective.  A group owns one context per local device and steps each local
+ * shard from its own host thread; counters, status, the first failing point (serial
+ * (tile, j, k, i) order over the whole domain) and diagnostics are combined on the host
+ * and, across processes, by one NCCL all-reduce group issued by the library (NCCL is
+ * dlopen'ed; single-process groups never load it).  Results per point do not depend on
+ * the decomposition in EXACT numerics (bitwise); in FAST numerics a point's rounding can
+ * depend on which points share its 16-point group, within the same 1e-12 bar. */
+enum { FSBM_SPLIT_I = 0, FSBM_SPLIT_J = 1 };
+
+/* split_range (driver.cpp:35-51) over i (i-slabs) or j (the WRF patches of decompose,
+ * driver.cpp:187-196): nshards near-equal ranges, remainder to the first, all k.
+ * FSBM_DOMAIN when nshards does not fit the extent (the reference's DomainError). */
+int fsbm_decompose(fsbm_ranges global, int nshards, int split, fsbm_ranges *shards_out);
+
+/* 128-byte ncclUniqueId for a multi-process group (rank 0 creates it, the caller
+ * broadcasts it, e.g. over torch.distributed or MPI). */
+int fsbm_nccl_unique_id(uint8_t id[128]);
+
+typedef struct fsbm_group fsbm_group;
+
+/* ndev local devices (repeats allowed: several shards on one GPU); this process is
+ * `rank` of `nranks` processes (1 for a single-process group; nccl_id may then be NULL).
+ * Table arguments as fsbm_ctx_create. */
+int fsbm_group_create(int ndev, const int *devices, int rank, int nranks, const uint8_t *nccl_id,
+                      int nkr, const double *x, double ratio, int npairs, const int *pair_abd,
+                      const double *t750, const double *t500, fsbm_group **out);
+int fsbm_group_destroy(fsbm_group *group);
+/* The context of local device `local` (device allocation, synthetic inputs, timing). */
+int fsbm_group_ctx(fsbm_group *group, int local, fsbm_ctx **ctx);
+
+/* One local shard of a device-resident domain: its global extents and its own arrays
+ * in GridState layout over those extents. */
+typedef struct {
+    fsbm_ranges ranges;
+    double *bins[FSBM_NCAT];
+    const double *pressure, *temperature;
+    const uint8_t *mask;
+    void *stream;
+} fsbm_shard;
+
+/* Reduced over every shard of every rank. */
+typedef struct {
+    double number_before[FSBM_NCAT], number_after[FSBM_NCAT];
+    double mass_before[FSBM_NCAT], mass_after[FSBM_NCAT];
+    float coal_kernel_ms_max;
+} fsbm_diag;
+
+/* fissioned_step over the group's shards (shards[ndev], device arrays): every output is
+ * the whole domain's, identical on every rank -- counters summed, the error that the
+ * serial reference would raise (earliest phase first, then the first failing point in
+ * (tile, j, k, i) order; tiles in global coordinates).  diag_out (nullable) adds two
+ * moment passes per shard. */
+int fsbm_group_step_device(fsbm_group *group, const fsbm_shard *shards, double dt, int substeps,
+                           const fsbm_plan *plan, const fsbm_tile *tiles, int ntiles,
+                           fsbm_counters *counters_out, fsbm_error *err_out, fsbm_diag *diag_out);
+
+/* fissioned_step on a host GridState spanning `global`: split into ndev*nranks i-slabs
+ * or j-patches; this process steps shards rank*ndev .. rank*ndev+ndev-1 in place
+ * (fsbm_step_patch_host, one host thread per device). */
+int fsbm_group_step_host(fsbm_group *group, fsbm_ranges global, int split,
+                         double *const bins_h[FSBM_NCAT], const double *pressure_h,
+                         const double *temperature_h, const uint8_t *mask_h, double dt,
+                         int substeps, const fsbm_plan *plan, const fsbm_tile *tiles, int ntiles,
+                         fsbm_counters *counters_out, fsbm_error *err_out);
+
+/* Max over all devices of all ranks of the coalescence kernel time of the last step. */
+int fsbm_group_last_timing(const fsbm_group *group, float *coal_kernel_ms_max);
 
 #ifdef __cplusplus
 }

@@ -251,7 +251,7 @@ int orc_synthetic_case(int ni, int nk, int nj, double cloud_fraction, uint64_t s
     int st = orc_mass_grid(nkr, x1, ratio, x);
     if (st) { free(x); return st; }
     const size_t np = (size_t)ni * nk * nj;
-    memset(bins, 0, sizeof(double) * ORC_NCAT * np * nkr);
+    if (bins) memset(bins, 0, sizeof(double) * ORC_NCAT * np * nkr); /* NULL: T/P only */
     const size_t n_cloudy = (size_t)llround(cloud_fraction * (double)np);
     uint64_t rng = seed;
     uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * np);
@@ -274,7 +274,7 @@ int orc_synthetic_case(int ni, int nk, int nj, double cloud_fraction, uint64_t s
             }
     const int kbar = nkr - 1 < nkr / 3 ? nkr - 1 : nkr / 3;
     const double xbar = x[kbar];
-    for (size_t p = 0; p < np && st == ORC_OK; ++p) {
+    for (size_t p = 0; bins && p < np && st == ORC_OK; ++p) {
         if (!cloudy[p]) continue;
         const double n_total = number_density * (0.5 + orc_uniform01(&rng));
         st = orc_exponential_init(nkr, x, n_total, xbar, bins + p * nkr); /* liquid = 0 */

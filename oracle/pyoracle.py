@@ -70,7 +70,7 @@ class Oracle:
         L.orc_uniform01.restype = C.c_double
         L.orc_synthetic_case.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                          C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp,
-                                         _dp]
+                                         C.c_void_p]
         L.orc_thunderstorm_point.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64, _dp]
         L.orc_thunderstorm_block.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64, C.c_uint64,
                                              C.c_void_p, _dp]
@@ -140,15 +140,18 @@ class Oracle:
         return st, cnt, (ec.value, eb.value)
 
     def synthetic_case(self, ni, nk, nj, cloud_fraction, seed, nkr=33, x1=3.35e-14, ratio=2.0,
-                       number_density=1e6):
+                       number_density=1e6, spectra=True):
+        """make_synthetic_case restated; spectra=False returns (T, P, None) without
+        allocating the 6 x npoints x nkr liquid-only spectra (same T/P bytes)."""
         np_ = ni * nk * nj
         T, P = np.zeros(np_), np.zeros(np_)
-        bins = np.zeros(NCAT * np_ * nkr)
+        bins = np.zeros(NCAT * np_ * nkr) if spectra else None
         st = self.lib.orc_synthetic_case(ni, nk, nj, cloud_fraction, seed, nkr, x1, ratio,
-                                         number_density, T, P, bins)
+                                         number_density, T, P,
+                                         bins.ctypes.data if spectra else None)
         if st:
             raise ValueError(f"synthetic_case status {st}")
-        return T, P, bins.reshape(NCAT, np_, nkr)
+        return T, P, (bins.reshape(NCAT, np_, nkr) if spectra else None)
 
     def thunderstorm_point(self, x, seed, p):
         out = np.zeros(NCAT * len(x))

@@ -6,5 +6,6 @@ include/fsbm_coal.h); ``coalbench`` mirrors the reference's host interface.
 from . import _lib
 from .coalbench import *  # noqa: F401,F403
 from .verify import *  # noqa: F401,F403
+from .group import DeviceGroup, GroupDiagnostics, nccl_unique_id  # noqa: F401
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -17,6 +17,7 @@ SO_PATH = os.environ.get("FSBM_LIB_PATH", SO_PATH)
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "fsbm_coal.h")
 
 NCAT = 6
+ABI_VERSION = 2
 
 
 class fsbm_ranges(C.Structure):
@@ -37,7 +38,19 @@ class fsbm_counters(C.Structure):
 
 
 class fsbm_error(C.Structure):
-    _fields_ = [(n, C.c_int) for n in ("category", "bin", "has_point", "i", "k", "j")]
+    _fields_ = [(n, C.c_int) for n in ("category", "bin", "has_point", "i", "k", "j")] + \
+        [("value", C.c_double)]
+
+
+class fsbm_shard(C.Structure):
+    _fields_ = [("ranges", fsbm_ranges), ("bins", C.c_void_p * NCAT), ("pressure", C.c_void_p),
+                ("temperature", C.c_void_p), ("mask", C.c_void_p), ("stream", C.c_void_p)]
+
+
+class fsbm_diag(C.Structure):
+    _fields_ = [("number_before", C.c_double * NCAT), ("number_after", C.c_double * NCAT),
+                ("mass_before", C.c_double * NCAT), ("mass_after", C.c_double * NCAT),
+                ("coal_kernel_ms_max", C.c_float)]
 
 
 class fsbm_field_diff(C.Structure):
@@ -61,6 +74,24 @@ _SIGS = {
     "fsbm_step_grid_host": ([_vp, fsbm_ranges, _vp * NCAT, _vp, _vp, _vp, C.c_double, C.c_int,
                              C.POINTER(fsbm_plan), _vp, C.c_int, C.POINTER(fsbm_counters),
                              C.POINTER(fsbm_error)], C.c_int),
+    "fsbm_step_patch_host": ([_vp, fsbm_ranges, fsbm_ranges, _vp * NCAT, _vp, _vp, _vp, C.c_double,
+                              C.c_int, C.POINTER(fsbm_plan), _vp, C.c_int,
+                              C.POINTER(fsbm_counters), C.POINTER(fsbm_error)], C.c_int),
+    "fsbm_state_moments_device": ([_vp, C.c_size_t, _vp * NCAT, C.c_double * (2 * NCAT), _vp],
+                                  C.c_int),
+    "fsbm_decompose": ([fsbm_ranges, C.c_int, C.c_int, C.POINTER(fsbm_ranges)], C.c_int),
+    "fsbm_nccl_unique_id": ([C.c_char * 128], C.c_int),
+    "fsbm_group_create": ([C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, _vp, C.c_int, _vp,
+                           C.c_double, C.c_int, _vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
+    "fsbm_group_destroy": ([_vp], C.c_int),
+    "fsbm_group_ctx": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
+    "fsbm_group_step_device": ([_vp, C.POINTER(fsbm_shard), C.c_double, C.c_int,
+                                C.POINTER(fsbm_plan), _vp, C.c_int, C.POINTER(fsbm_counters),
+                                C.POINTER(fsbm_error), C.POINTER(fsbm_diag)], C.c_int),
+    "fsbm_group_step_host": ([_vp, fsbm_ranges, C.c_int, _vp * NCAT, _vp, _vp, _vp, C.c_double,
+                              C.c_int, C.POINTER(fsbm_plan), _vp, C.c_int,
+                              C.POINTER(fsbm_counters), C.POINTER(fsbm_error)], C.c_int),
+    "fsbm_group_last_timing": ([_vp, C.POINTER(C.c_float)], C.c_int),
     "fsbm_coal_step": ([_vp, _vp, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                         C.POINTER(fsbm_counters), C.POINTER(fsbm_error)], C.c_int),
     "fsbm_synth_thermo_host": ([C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, _vp,
@@ -102,7 +133,7 @@ def load(path: str = SO_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.fsbm_abi_version() != 1:
+    if lib.fsbm_abi_version() != ABI_VERSION:
         raise RuntimeError("libfsbm_coal.so ABI version mismatch")
     _lib = lib
     return lib
@@ -126,11 +157,12 @@ class ConfigError(Error):
 
 
 class StiffnessError(Error):
-    def __init__(self, msg, category=-1, bin=-1, point=None):
+    def __init__(self, msg, category=-1, bin=-1, point=None, value=None):
         super().__init__(msg)
         self.category = category
         self.bin = bin
         self.point = point  # (i, k, j) 1-based, or None
+        self.value = value  # the negative bin value of the message
 
     def has_point(self):
         return self.point is not None
@@ -155,5 +187,6 @@ def check(status: int, err: fsbm_error | None = None) -> None:
     cls = _STATUS.get(status, Error)
     if cls is StiffnessError:
         point = (err.i, err.k, err.j) if err is not None and err.has_point else None
-        raise StiffnessError(msg, err.category if err else -1, err.bin if err else -1, point)
+        raise StiffnessError(msg, err.category if err else -1, err.bin if err else -1, point,
+                             err.value if err is not None else None)
     raise cls(msg)

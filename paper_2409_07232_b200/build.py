@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT_DIR, "libfsbm_coal.so")
 SOURCES = ["fsbm_coal.cu"]
-HEADERS = ["fsbm_common.cuh", "coal_exact.cuh", "coal_fast.cuh", "coal_dmma.cuh", "coal_dmmag.cuh", "state_io.cuh"]
+HEADERS = ["fsbm_common.cuh", "coal_exact.cuh", "coal_fast.cuh", "coal_dmma.cuh", "coal_dmmag.cuh", "state_io.cuh", "fsbm_group.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [NVCC] + ARCH + FLAGS + [os.path.join(CSRC, f) for f in SOURCES] + ["-o", SO + ".tmp"]
+    cmd = [NVCC] + ARCH + FLAGS + [os.path.join(CSRC, f) for f in SOURCES] + ["-o", SO + ".tmp", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(OUT_DIR, "build.log")
     with open(log, "w") as fh:

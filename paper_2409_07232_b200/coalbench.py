@@ -439,6 +439,55 @@ def fission_predicates(state: GridState, ctx: Optional[CoalContext] = None) -> P
     return PredicateMask(state.ranges, on.astype(np.uint8), int(on.sum()))
 
 
+def _check_buffers(state: GridState, mask: Optional[PredicateMask], ctx: CoalContext) -> None:
+    """The C ABI trusts npoints*nkr doubles per category: check dtype, size, contiguity
+    and placement of every buffer before handing raw pointers over (ShapeError /
+    DomainError, as the reference's GridState/PredicateMask checks, driver.cpp:127-129)."""
+    np_ = state.ranges.npoints()
+    dev = state.on_device()
+
+    def check(a, name, dtype, n):
+        if a is None:
+            return
+        if _is_cuda(a) != dev:
+            raise DomainError(f"fissioned_step: {name} is {'host' if dev else 'device'} memory "
+                              f"but the state is on the {'device' if dev else 'host'}")
+        if dev:
+            import torch
+            tdt = {np.float64: torch.float64, np.uint8: torch.uint8}[dtype]
+            if a.dtype != tdt:
+                raise ShapeError(f"fissioned_step: {name} must be {tdt}, got {a.dtype}")
+            if not a.is_contiguous():
+                raise ShapeError(f"fissioned_step: {name} must be contiguous")
+            if a.device.index != ctx.device:
+                raise DomainError(f"fissioned_step: {name} is on cuda:{a.device.index}, "
+                                  f"the context on cuda:{ctx.device}")
+            size = a.numel()
+        else:
+            if not isinstance(a, np.ndarray):
+                raise ShapeError(f"fissioned_step: {name} must be a numpy array")
+            if a.dtype != dtype:
+                raise ShapeError(f"fissioned_step: {name} must be {np.dtype(dtype)}, got {a.dtype}")
+            if not a.flags.c_contiguous:
+                raise ShapeError(f"fissioned_step: {name} must be C-contiguous")
+            size = a.size
+        if size != n:
+            raise ShapeError(f"fissioned_step: {name} has {size} elements, expected {n}")
+
+    if len(state.bins) != NCAT:
+        raise ShapeError(f"fissioned_step: state needs {NCAT} category arrays")
+    for c, b in enumerate(state.bins):
+        if b is None:
+            raise DomainError("fissioned_step: null category array")
+        check(b, f"bins[{CATEGORIES[c]}]", np.float64, np_ * state.nkr())
+    if state.pressure is None:
+        raise DomainError("fissioned_step: pressure is required")
+    check(state.pressure, "pressure", np.float64, np_)
+    check(state.temperature, "temperature", np.float64, np_)
+    if mask is not None:
+        check(mask.call_coal, "mask", np.uint8, np_)
+
+
 def fissioned_step(state: GridState, mask: Optional[PredicateMask], step: StepContext,
                    plan: ExecPlan = ExecPlan()) -> None:
     """fissioned_step (driver.hpp:179-180, driver.cpp:353-434) -- phase 2 on the GPU.
@@ -453,6 +502,7 @@ def fissioned_step(state: GridState, mask: Optional[PredicateMask], step: StepCo
         raise ShapeError("fissioned_step: mask extents do not match the state")
     if state.nkr() != ctx.nkr:
         raise ShapeError("coal_step: state distribution size does not match nkr")
+    _check_buffers(state, mask, ctx)
     cplan = plan.to_c()
     tiles = step.tiles.tiles if step.tiles is not None else []
     tarr = (fsbm_tile * max(1, len(tiles)))(*[fsbm_tile(*t) for t in tiles])

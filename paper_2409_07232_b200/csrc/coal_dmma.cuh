@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         const uint32_t p = pidx[q];
                         if (p == 0xffffffffu || pfail[q] != 0) continue;
                         if (W(c, k, q) < 0.0) {
-                            report_stiffness(A, p, c, k);
+                            report_stiffness(A, p, c, k, W(c, k, q));
                             pfail[q] = 2;
                         }
                     }

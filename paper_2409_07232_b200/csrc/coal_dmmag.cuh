@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         const uint32_t p = pidx[q];
                         if (p == 0xffffffffu || pfail[q] != 0) continue;
                         if (W(c, k, q) < 0.0) {
-                            report_stiffness(A, p, c, k);
+                            report_stiffness(A, p, c, k, W(c, k, q));
                             pfail[q] = 2;
                         }
                     }

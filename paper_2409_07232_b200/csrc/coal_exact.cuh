@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, d
                 for (int k = 0; k < nkr; ++k) {
                     const double v = __dadd_rn(W[(c * nkr + k) * L], Dl[(c * nkr + k) * L]);
                     if (v < 0.0) {
-                        report_stiffness(A, p, c, k);
+                        report_stiffness(A, p, c, k, v);
                         failed = true;
                         break;
                     }

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
                     const double v = work[ix] + (delta[ix] + dhi[ix]);
                     work[ix] = v;
                     if (v < 0.0 && pfail[qi] == 0) {
-                        report_stiffness(A, p, c, k);
+                        report_stiffness(A, p, c, k, v);
                         pfail[qi] = 2; // first failing substep marks the point
                     }
                 }

@@ -94,7 +94,8 @@ struct fsbm_ctx {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     double *d_arena = nullptr;
     size_t arena_bytes = 0;
-    unsigned long long *d_sink = nullptr;  // {err_key, triples, points, evals, count}
+    // {err_key, triples, points, evals, stale, predicate count, err value bits, err lock}
+    unsigned long long *d_sink = nullptr;
     unsigned long long *h_sink = nullptr;  // pinned mirror
     int4 *d_tiles = nullptr;
     int tiles_cap = 0;
@@ -310,7 +311,7 @@ int validate_step(fsbm_ctx *c, fsbm_ranges r, const double *P, const double *T,
 }
 
 int begin_step(fsbm_ctx *c, cudaStream_t s) {
-    static const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
+    static const unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
     FSBM_CUDA_TRY(cudaMemcpyAsync(c->d_sink, init, sizeof(init), cudaMemcpyHostToDevice, s));
     c->timed = false;
     c->last_launches = 0;
@@ -372,6 +373,7 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     A.g_whi = c->d_gwhi;
     A.g_top = c->d_gtop;
     A.err_key = c->d_sink;
+    A.err_aux = c->d_sink + 6;
     A.counters = c->d_sink + 1;
     A.tiles = tl;
     A.ntiles = ntiles;
@@ -405,14 +407,21 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     return FSBM_OK;
 }
 
+/// StiffnessError's text (coalescence.cpp:319-325), value formatted by std::to_string.
+std::string stiffness_message(int cat, int bin, double v) {
+    static const char *names[FSBM_NCAT] = {"liquid", "ice1", "ice2", "ice3", "snow", "graupel"};
+    return "coal_step: bin " + std::to_string(bin) + " of category " + names[cat] +
+           " would become negative (" + std::to_string(v) + "); reduce dt or increase substeps";
+}
+
 /// One sync, then counters / stale / stiffness from the sink.
 int finalize_step(fsbm_ctx *c, const StepGeom &g, cudaStream_t s, fsbm_counters *counters_out,
                   fsbm_error *err_out) {
-    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink, c->d_sink, 5 * sizeof(unsigned long long),
+    FSBM_CUDA_TRY(cudaMemcpyAsync(c->h_sink, c->d_sink, 8 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
     FSBM_CUDA_TRY(cudaStreamSynchronize(s));
     if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
-    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0, 0.0};
     if (c->h_sink[4] != 0)
         return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
                                  "temperatures (stale predicate)");
@@ -425,13 +434,12 @@ int finalize_step(fsbm_ctx *c, const StepGeom &g, cudaStream_t s, fsbm_counters 
     const int i = static_cast<int>(in_tile % g.ni);
     const int k = static_cast<int>((in_tile / g.ni) % g.nk);
     const int j = static_cast<int>(in_tile / (static_cast<unsigned long long>(g.ni) * g.nk));
-    static const char *names[FSBM_NCAT] = {"liquid", "ice1", "ice2", "ice3", "snow", "graupel"};
-    if (err_out) *err_out = fsbm_error{cat, bin, 1, i + g.r.ids, k + g.r.kds, j + g.r.jds};
-    return fail(FSBM_STIFFNESS,
-                "coal_step: bin " + std::to_string(bin) + " of category " + names[cat] +
-                    " would become negative; reduce dt or increase substeps at grid point (i=" +
-                    std::to_string(i + g.r.ids) + ", k=" + std::to_string(k + g.r.kds) +
-                    ", j=" + std::to_string(j + g.r.jds) + ")");
+    double v;
+    std::memcpy(&v, &c->h_sink[6], sizeof v);
+    if (err_out) *err_out = fsbm_error{cat, bin, 1, i + g.r.ids, k + g.r.kds, j + g.r.jds, v};
+    return fail(FSBM_STIFFNESS, stiffness_message(cat, bin, v) + " at grid point (i=" +
+                                    std::to_string(i + g.r.ids) + ", k=" + std::to_string(k + g.r.kds) +
+                                    ", j=" + std::to_string(j + g.r.jds) + ")");
 }
 
 /// coal_step's argument checks (coalescence.cpp:206-209) fire only when a point runs;
@@ -517,6 +525,53 @@ __global__ void thunderstorm_kernel(size_t np, uint64_t offset, int nkr, const d
             for (int k = 0; k < nkr; ++k) out[k] = __dmul_rn(n_total, out[k] / wsum);
         }
     }
+}
+
+// ---- state moments (diagnostics) ---------------------------------------------
+// Per category sum_p sum_k n and sum_p sum_k n*x[k] over a flat [np*nkr] array: each
+// thread walks the flat array (coalesced), block tree reduction, one partial per block;
+// a single block then sums the partials in a fixed order (deterministic run to run).
+constexpr int kMomThreads = 256;
+
+__global__ void __launch_bounds__(kMomThreads) moments_kernel(size_t n, int nkr, const double *x,
+                                                              const double *b, double *partial) {
+    __shared__ double sh[2][kMomThreads / 32];
+    double sn = 0.0, sm = 0.0;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double v = b[e];
+        sn += v;
+        sm = fma(v, __ldg(x + e % nkr), sm);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sn += __shfl_down_sync(0xffffffffu, sn, o);
+        sm += __shfl_down_sync(0xffffffffu, sm, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = sn;
+        sh[1][threadIdx.x >> 5] = sm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, m = 0.0;
+        for (int w = 0; w < kMomThreads / 32; ++w) {
+            a += sh[0][w];
+            m += sh[1][w];
+        }
+        partial[2 * blockIdx.x] = a;
+        partial[2 * blockIdx.x + 1] = m;
+    }
+}
+
+__global__ void moments_final_kernel(int nblocks, const double *partial, double *out) {
+    if (threadIdx.x != 0) return;
+    double a = 0.0, m = 0.0;
+    for (int q = 0; q < nblocks; ++q) {
+        a += partial[2 * q];
+        m += partial[2 * q + 1];
+    }
+    out[0] = a;
+    out[1] = m;
 }
 
 // ---- FP64 roof probe --------------------------------------------------------
@@ -685,7 +740,7 @@ int fsbm_step_grid_device(fsbm_ctx *c, fsbm_ranges ranges, double *const bins_d[
     if (int st = check_step_args(c, g, mask_d, temperature_d, ntiles, dt, substeps, s, &nothing))
         return st;
     if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
-    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+    if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0, 0.0};
     if (nothing) return FSBM_OK;
     if (int st = begin_step(c, s)) return st;
     if (int st = enqueue_chunk(c, 0, g, 0, g.ni, bins_d, pressure_d, temperature_d, mask_d, dt,
@@ -699,6 +754,15 @@ int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NC
                         const uint8_t *mask_h, double dt, int substeps, const fsbm_plan *plan_in,
                         const fsbm_tile *tiles, int ntiles, fsbm_counters *counters_out,
                         fsbm_error *err_out) {
+    return fsbm_step_patch_host(c, r, r, bins_h, pressure_h, temperature_h, mask_h, dt, substeps,
+                                plan_in, tiles, ntiles, counters_out, err_out);
+}
+
+int fsbm_step_patch_host(fsbm_ctx *c, fsbm_ranges gr, fsbm_ranges r,
+                         double *const bins_h[FSBM_NCAT], const double *pressure_h,
+                         const double *temperature_h, const uint8_t *mask_h, double dt,
+                         int substeps, const fsbm_plan *plan_in, const fsbm_tile *tiles,
+                         int ntiles, fsbm_counters *counters_out, fsbm_error *err_out) {
     if (!c) return fail(FSBM_DOMAIN, "fissioned_step: context must supply tables and gains");
     DeviceGuard dg(c->device);
     fsbm_plan plan_default{0, 2, 1, FSBM_ON_DEMAND, FSBM_AUTOMATIC, FSBM_NUMERICS_FAST};
@@ -706,34 +770,62 @@ int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NC
     StepGeom g{};
     if (int st = validate_step(c, r, pressure_h, temperature_h, mask_h, plan, tiles, ntiles, g))
         return st;
+    if (gr.ide < gr.ids || gr.kde < gr.kds || gr.jde < gr.jds)
+        return fail(FSBM_SHAPE, "fissioned_step: empty or inverted ranges");
+    if (r.ids < gr.ids || r.ide > gr.ide || r.jds < gr.jds || r.jde > gr.jde ||
+        r.kds != gr.kds || r.kde != gr.kde)
+        return fail(FSBM_SHAPE, "fissioned_step: patch is not an i/j sub-range (all k) of the "
+                                "state's ranges");
     for (int q = 0; q < FSBM_NCAT; ++q)
         if (!bins_h[q]) return fail(FSBM_DOMAIN, "fissioned_step: null category array");
     const int nkr = c->nkr;
     const size_t per_i = static_cast<size_t>(g.nk) * g.nj;
+    // the host arrays span gr; the patch's point (i,k,j) sits at line (i*nk + k) of pitch nj_g
+    const size_t nj_g = static_cast<size_t>(gr.jde - gr.jds + 1);
+    const size_t di = static_cast<size_t>(r.ids - gr.ids), dj = static_cast<size_t>(r.jds - gr.jds);
+    const bool pitched = nj_g != static_cast<size_t>(g.nj);
+    auto gidx = [&](size_t p) { // patch-local point -> index into the host arrays
+        const size_t line = p / g.nj, j = p % g.nj;
+        return ((di * g.nk) + line) * nj_g + dj + j;
+    };
     // Host-side stale check first: the reference raises before touching any point.
     if (mask_h && temperature_h)
         for (size_t p = 0; p < g.np; ++p) {
-            const double t = temperature_h[p];
-            if ((t > kOuterGateK && t > kCoalGateK) != (mask_h[p] != 0))
+            const size_t q = gidx(p);
+            const double t = temperature_h[q];
+            if ((t > kOuterGateK && t > kCoalGateK) != (mask_h[q] != 0))
                 return fail(FSBM_DOMAIN, "fissioned_step: mask is inconsistent with the state's "
                                          "temperatures (stale predicate)");
         }
     if (!(dt > 0.0) || substeps < 1) {
+        // coal_step's checks fire only if some point inside the tile plan runs
+        // (the device path's count_active_sync applies the same tile test)
         size_t n = 0;
         for (size_t p = 0; p < g.np; ++p) {
-            const bool on = mask_h ? mask_h[p] != 0
-                                   : (temperature_h[p] > kOuterGateK && temperature_h[p] > kCoalGateK);
+            const size_t q = gidx(p);
+            bool on = mask_h ? mask_h[q] != 0
+                             : (temperature_h[q] > kOuterGateK && temperature_h[q] > kCoalGateK);
+            if (on && ntiles > 0) {
+                const int gi = static_cast<int>(p / per_i) + r.ids;
+                const int gj = static_cast<int>(p % g.nj) + r.jds;
+                bool in = false;
+                for (int t = 0; t < ntiles && !in; ++t)
+                    in = gi >= tiles[t].its && gi <= tiles[t].ite && gj >= tiles[t].jts &&
+                         gj <= tiles[t].jte;
+                on = in;
+            }
             n += on;
         }
         if (counters_out) *counters_out = fsbm_counters{0, 0, 0};
-        if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0};
+        if (err_out) *err_out = fsbm_error{-1, -1, 0, 0, 0, 0, 0.0};
         if (n == 0) return FSBM_OK;
         return fail(FSBM_DOMAIN, !(dt > 0.0) ? "coal_step: dt must be > 0" : "coal_step: substeps must be >= 1");
     }
     // Pipeline over i-chunks: H2D (s_in) -> flags/compaction/kernel (stream) -> D2H
     // (s_out), kSlots chunks in flight; pinned host memory makes the copies async.
     // ~192 MB chunks: pipeline fill (first H2D) and drain (last kernel + D2H) stay a few
-    // percent of the step while the copy engines run H2D and D2H concurrently.
+    // percent of the step while the copy engines run H2D and D2H concurrently.  A j-patch
+    // of a wider state moves (i,k) lines with pitched 2-D copies (no host-side gather).
     const size_t row_bytes = per_i * (FSBM_NCAT * static_cast<size_t>(nkr) * sizeof(double) + 17);
     const int rows = static_cast<int>(std::max<size_t>(1, std::min<size_t>(g.ni, (192u << 20) / row_bytes)));
     const size_t chunk_np = static_cast<size_t>(rows) * per_i;
@@ -750,14 +842,38 @@ int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NC
             c->chunk_bytes[k] = need;
         }
     cudaStream_t sc = c->stream;
+    // Any return from here on (error paths included) first drains all three pipeline
+    // streams, so no copy into the caller's buffers is still in flight afterwards.
+    struct Drain {
+        fsbm_ctx *c;
+        ~Drain() {
+            cudaStreamSynchronize(c->s_in);
+            cudaStreamSynchronize(c->stream);
+            cudaStreamSynchronize(c->s_out);
+        }
+    } drain{c};
+    // (elements per point) -> copy `lines` lines of the patch starting at patch line l0
+    auto copy = [&](void *dst, const void *src_base, size_t elem, size_t l0, size_t lines,
+                    cudaMemcpyKind kind, cudaStream_t st, bool to_host) -> cudaError_t {
+        const size_t w = g.nj * elem, sp = nj_g * elem;
+        char *hb = static_cast<char *>(const_cast<void *>(src_base)) +
+                   (((di * g.nk) + l0) * nj_g + dj) * elem;
+        if (!pitched) {
+            return to_host ? cudaMemcpyAsync(hb, dst, lines * w, kind, st)
+                           : cudaMemcpyAsync(dst, hb, lines * w, kind, st);
+        }
+        return to_host ? cudaMemcpy2DAsync(hb, sp, dst, w, w, lines, kind, st)
+                       : cudaMemcpy2DAsync(dst, w, hb, sp, w, lines, kind, st);
+    };
     if (int st = begin_step(c, sc)) return st;
     FSBM_CUDA_TRY(cudaEventRecord(c->ev_comp[0], sc)); // sink init precedes every chunk
     FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_in, c->ev_comp[0]));
+    const size_t pt_bins = static_cast<size_t>(nkr) * sizeof(double);
     int k = 0;
     for (int i0 = 0; i0 < g.ni; i0 += rows, ++k) {
         const int i1 = std::min(g.ni, i0 + rows);
         const int slot = k % fsbm_ctx::kSlots;
-        const size_t p0 = static_cast<size_t>(i0) * per_i, np = static_cast<size_t>(i1 - i0) * per_i;
+        const size_t l0 = static_cast<size_t>(i0) * g.nk, lines = static_cast<size_t>(i1 - i0) * g.nk;
         char *base = reinterpret_cast<char *>(c->d_chunk[slot]);
         double *bd[FSBM_NCAT];
         for (int q = 0; q < FSBM_NCAT; ++q)
@@ -767,26 +883,22 @@ int fsbm_step_grid_host(fsbm_ctx *c, fsbm_ranges r, double *const bins_h[FSBM_NC
         uint8_t *Md = reinterpret_cast<uint8_t *>(Td + chunk_np);
         if (k >= fsbm_ctx::kSlots) FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_in, c->ev_out[slot]));
         for (int q = 0; q < FSBM_NCAT; ++q)
-            FSBM_CUDA_TRY(cudaMemcpyAsync(bd[q], bins_h[q] + p0 * nkr, np * nkr * sizeof(double),
-                                          cudaMemcpyHostToDevice, c->s_in));
-        FSBM_CUDA_TRY(cudaMemcpyAsync(Pd, pressure_h + p0, np * sizeof(double), cudaMemcpyHostToDevice, c->s_in));
+            FSBM_CUDA_TRY(copy(bd[q], bins_h[q], pt_bins, l0, lines, cudaMemcpyHostToDevice, c->s_in, false));
+        FSBM_CUDA_TRY(copy(Pd, pressure_h, sizeof(double), l0, lines, cudaMemcpyHostToDevice, c->s_in, false));
         if (temperature_h)
-            FSBM_CUDA_TRY(cudaMemcpyAsync(Td, temperature_h + p0, np * sizeof(double),
-                                          cudaMemcpyHostToDevice, c->s_in));
-        if (mask_h) FSBM_CUDA_TRY(cudaMemcpyAsync(Md, mask_h + p0, np, cudaMemcpyHostToDevice, c->s_in));
+            FSBM_CUDA_TRY(copy(Td, temperature_h, sizeof(double), l0, lines, cudaMemcpyHostToDevice,
+                               c->s_in, false));
+        if (mask_h) FSBM_CUDA_TRY(copy(Md, mask_h, 1, l0, lines, cudaMemcpyHostToDevice, c->s_in, false));
         FSBM_CUDA_TRY(cudaEventRecord(c->ev_in[slot], c->s_in));
         FSBM_CUDA_TRY(cudaStreamWaitEvent(sc, c->ev_in[slot]));
         if (int st = enqueue_chunk(c, slot, g, i0, i1, bd, Pd, temperature_h ? Td : nullptr,
                                    mask_h ? Md : nullptr, dt, substeps, plan, ntiles, sc, k == 0,
-                                   i1 == g.ni)) {
-            cudaStreamSynchronize(sc);
+                                   i1 == g.ni))
             return st;
-        }
         FSBM_CUDA_TRY(cudaEventRecord(c->ev_comp[slot], sc));
         FSBM_CUDA_TRY(cudaStreamWaitEvent(c->s_out, c->ev_comp[slot]));
         for (int q = 0; q < FSBM_NCAT; ++q)
-            FSBM_CUDA_TRY(cudaMemcpyAsync(bins_h[q] + p0 * nkr, bd[q], np * nkr * sizeof(double),
-                                          cudaMemcpyDeviceToHost, c->s_out));
+            FSBM_CUDA_TRY(copy(bd[q], bins_h[q], pt_bins, l0, lines, cudaMemcpyDeviceToHost, c->s_out, true));
         FSBM_CUDA_TRY(cudaEventRecord(c->ev_out[slot], c->s_out));
     }
     FSBM_CUDA_TRY(cudaStreamSynchronize(c->s_out));
@@ -812,11 +924,10 @@ int fsbm_coal_step(fsbm_ctx *c, double *bins6, double pressure, double dt, int s
         *err_out = e;
         err_out->has_point = 0; // coal_step itself reports no coordinates
     }
-    if (st == FSBM_STIFFNESS) {
-        static const char *names[FSBM_NCAT] = {"liquid", "ice1", "ice2", "ice3", "snow",
-                                               "graupel"};
-        g_err = "coal_step: bin " + std::to_string(e.bin) + " of category " + names[e.category] +
-                " would become negative; reduce dt or increase substeps";
+    if (st == FSBM_STIFFNESS) { // coal_step itself reports no coordinates
+        double v;
+        std::memcpy(&v, &c->h_sink[6], sizeof v);
+        g_err = stiffness_message(e.category, e.bin, v);
     }
     return st;
 }
@@ -895,6 +1006,39 @@ int fsbm_synth_thunderstorm_device(fsbm_ctx *c, size_t npoints, uint64_t point_o
     return FSBM_OK;
 }
 
+int fsbm_state_moments_device(fsbm_ctx *c, size_t npoints, const double *const bins_d[FSBM_NCAT],
+                              double out[2 * FSBM_NCAT], void *stream) {
+    if (!c || !out) return fail(FSBM_DOMAIN, "state moments: null argument");
+    for (int q = 0; q < FSBM_NCAT; ++q)
+        if (!bins_d[q]) return fail(FSBM_DOMAIN, "state moments: null category array");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = npoints * static_cast<size_t>(c->nkr);
+    const int blocks = static_cast<int>(std::min<size_t>(std::max<size_t>((n + kMomThreads - 1) / kMomThreads, 1),
+                                                         static_cast<size_t>(c->num_sms) * 8));
+    // workspace: blocks partials per category + 12 results (slot 2 of the compaction ws,
+    // which no step uses concurrently with this call on the same context)
+    const size_t need = (static_cast<size_t>(FSBM_NCAT) * blocks * 2 + 2 * FSBM_NCAT) * sizeof(double);
+    if (int st = ensure_ws(c, fsbm_ctx::kSlots - 1, need)) return st;
+    double *ws = static_cast<double *>(c->d_ws[fsbm_ctx::kSlots - 1]);
+    double *res = ws + static_cast<size_t>(FSBM_NCAT) * blocks * 2;
+    for (int q = 0; q < FSBM_NCAT; ++q) {
+        moments_kernel<<<blocks, kMomThreads, 0, s>>>(n, c->nkr, c->d_x, bins_d[q],
+                                                      ws + static_cast<size_t>(q) * blocks * 2);
+        moments_final_kernel<<<1, 32, 0, s>>>(blocks, ws + static_cast<size_t>(q) * blocks * 2,
+                                              res + 2 * q);
+    }
+    FSBM_CUDA_TRY(cudaGetLastError());
+    double tmp[2 * FSBM_NCAT];
+    FSBM_CUDA_TRY(cudaMemcpyAsync(tmp, res, sizeof(tmp), cudaMemcpyDeviceToHost, s));
+    FSBM_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int q = 0; q < FSBM_NCAT; ++q) {
+        out[q] = tmp[2 * q];
+        out[FSBM_NCAT + q] = tmp[2 * q + 1];
+    }
+    return FSBM_OK;
+}
+
 int fsbm_probe_fp64_peak(int device, double *tflops) {
     if (!tflops) return fail(FSBM_DOMAIN, "null output");
     DeviceGuard g(device);
@@ -951,3 +1095,4 @@ int fsbm_ctx_last_timing(const fsbm_ctx *c, float *coal_kernel_ms, int *launches
 } // extern "C"
 
 #include "state_io.cuh"
+#include "fsbm_group.cuh"

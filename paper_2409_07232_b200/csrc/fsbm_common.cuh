@@ -51,6 +51,7 @@ struct StepArgs {
     const double *g_wlo, *g_whi, *g_top;
     // error / counter sink
     unsigned long long *err_key;   // min over failing points of (order<<20 | c*nkr+bin)
+    unsigned long long *err_aux;   // {bits of the winning point's negative value, lock}
     unsigned long long *counters;  // {triples, points, kernel_evals}
     const int4 *tiles;             // (its, ite, jts, jte) 1-based, or null
     int ntiles;
@@ -74,9 +75,23 @@ __device__ inline unsigned long long order_key(const StepArgs &A, uint32_t p) {
     return t * np + ((unsigned long long)j * A.nk + k) * A.ni_glob + i;
 }
 
-__device__ inline void report_stiffness(const StepArgs &A, uint32_t p, int c, int bin) {
+/// Records (key, value) if key is the smallest so far.  The value rides with the key
+/// (the reference's message prints it, coalescence.cpp:319-325), so the pair is updated
+/// under a tiny spin lock: this is the error path only, a failing step takes it a
+/// handful of times.
+__device__ inline void report_stiffness(const StepArgs &A, uint32_t p, int c, int bin, double v) {
     const unsigned long long key = (order_key(A, p) << 20) | (unsigned long long)(c * A.nkr + bin);
-    atomicMin(A.err_key, key);
+    volatile unsigned long long *vk = A.err_key;
+    if (key >= *vk) return;
+    while (atomicCAS(A.err_aux + 1, 0ull, 1ull) != 0ull) __nanosleep(64);
+    __threadfence();
+    if (key < *vk) {
+        *vk = key;
+        *reinterpret_cast<volatile unsigned long long *>(A.err_aux) =
+            static_cast<unsigned long long>(__double_as_longlong(v));
+    }
+    __threadfence();
+    atomicExch(A.err_aux + 1, 0ull);
 }
 
 } // namespace fsbm

@@ -14,16 +14,28 @@ from dataclasses import dataclass
 import numpy as np
 
 
+def decompose_shards(ranges, nshards: int, split: str = "i") -> list:
+    """fsbm_decompose (C ABI; split_range, driver.cpp:35-51): nshards near-equal i-slabs
+    ("i") or WRF j-patches ("j", decompose, driver.cpp:187-196) of `ranges`, all k."""
+    import ctypes as C
+
+    from . import _lib
+    from .coalbench import Ranges
+    out = (_lib.fsbm_ranges * max(1, nshards))()
+    _lib.check(_lib.load().fsbm_decompose(ranges.to_c(), nshards, {"i": 0, "j": 1}[split], out))
+    return [Ranges(o.ids, o.ide, o.kds, o.kde, o.jds, o.jde) for o in out[:nshards]]
+
+
 def slab(ni: int, world: int, rank: int) -> tuple[int, int]:
-    """Near-equal split of [0, ni) (sizes differ by <= 1, remainder to the first
-    ranks), as decompose's split_range (driver.cpp:35-51).  Returns (i0, i1)."""
+    """Rank's i-slab of [0, ni) (sizes differ by <= 1, remainder to the first ranks), from
+    fsbm_decompose.  Returns (i0, i1), 0-based half-open."""
+    from .coalbench import Ranges
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     if ni < world:
         raise ValueError(f"cannot split {ni} i-rows over {world} ranks")
-    base, rem = divmod(ni, world)
-    i0 = rank * base + min(rank, rem)
-    return i0, i0 + base + (1 if rank < rem else 0)
+    r = decompose_shards(Ranges(1, ni, 1, 1, 1, 1), world, "i")[rank]
+    return r.ids - 1, r.ide
 
 
 def shard_slice(ni: int, nk: int, nj: int, world: int, rank: int) -> tuple[int, int]:

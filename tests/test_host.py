@@ -85,3 +85,70 @@ def test_pressure_weight_and_interp():
     assert fsbm.pressure_weight(625.0) == 0.5
     assert fsbm.interpolate_kernel(3.0, 4.5, 0.5) == 3.75
     assert fsbm.pressure_weight(100.0) == 0.0 and fsbm.pressure_weight(1000.0) == 1.0
+
+
+def test_decompose_shards_match_reference_decompose():
+    """fsbm_decompose (C ABI) == decompose's split_range (driver.cpp:35-51,187-196)."""
+    from paper_2409_07232_b200 import shard
+    r = fsbm.Ranges(1, 425, 1, 50, 1, 300)
+    for n in (1, 2, 3, 4, 8, 7):
+        jp = shard.decompose_shards(r, n, "j")
+        ref = fsbm.decompose(r, n, 1).tiles  # (its, ite, jts, jte), one tile per patch
+        assert [(p.jds, p.jde) for p in jp] == [(t[2], t[3]) for t in ref]
+        assert all((p.ids, p.ide, p.kds, p.kde) == (1, 425, 1, 50) for p in jp)
+        ip = shard.decompose_shards(r, n, "i")
+        ref = fsbm.decompose(r, 1, n).tiles
+        assert [(p.ids, p.ide) for p in ip] == [(t[0], t[1]) for t in ref]
+    with pytest.raises(fsbm.DomainError):
+        shard.decompose_shards(fsbm.Ranges(1, 3, 1, 1, 1, 2), 3, "j")
+    with pytest.raises(fsbm.ConfigError):
+        _lib.check(_lib.load().fsbm_decompose(r.to_c(), 2, 5, (_lib.fsbm_ranges * 2)()))
+
+
+def test_fissioned_step_validates_buffers():
+    """dtype / size / contiguity / placement are checked before any raw pointer
+    reaches the C ABI (ShapeError / DomainError, no out-of-bounds access)."""
+    grid = fsbm.make_mass_grid(33)
+    r = fsbm.Ranges(1, 2, 1, 2, 1, 2)
+    n = r.npoints()
+    good = lambda: [np.zeros(n * 33) for _ in range(6)]
+    T, P = np.full(n, 250.0), np.full(n, 600.0)
+
+    class _Ctx:  # validation runs before any library call
+        nkr, device = 33, 0
+    sctx = fsbm.StepContext(_Ctx())
+    cases = [
+        (fsbm.GridState(r, grid, T, P, [b.astype(np.float32) for b in good()]), None, fsbm.ShapeError),
+        (fsbm.GridState(r, grid, T, P, [np.zeros(n * 33 - 1)] + good()[1:]), None, fsbm.ShapeError),
+        (fsbm.GridState(r, grid, T, P[:-1], good()), None, fsbm.ShapeError),
+        (fsbm.GridState(r, grid, T, P, [np.zeros((n * 33, 2))[:, 0]] + good()[1:]), None, fsbm.ShapeError),
+        (fsbm.GridState(r, grid, T, P, good()), fsbm.PredicateMask(r, np.zeros(n, np.int32)), fsbm.ShapeError),
+        (fsbm.GridState(r, grid, T, None, good()), None, fsbm.DomainError),
+        (fsbm.GridState(r, grid, T, P, good()[:5]), None, fsbm.ShapeError),
+    ]
+    for st, m, exc in cases:
+        with pytest.raises(exc):
+            fsbm.fissioned_step(st, m, sctx, fsbm.ExecPlan())
+
+
+def test_bench_reference_arm_never_loads_the_product(tmp_path):
+    """The reference arm (bench.py --impl reference) runs oracle/_ref on inputs from the
+    checkers only: no paper_2409_07232_b200 import, no libfsbm_coal.so mapping."""
+    import json
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--ni', '3', "
+            "'--nj', '8', '--nk', '5', '--steps', '1', '--warmup', '1']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT', any(m.startswith('paper_2409') for m in sys.modules), "
+            "'libfsbm_coal' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    line = json.loads(lines[-2])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
+    assert lines[-1] == "PRODUCT False False"

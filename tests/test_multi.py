@@ -1,6 +1,8 @@
-"""N>1 path on CPU: world_size-2 gloo process group, i-slab shards, the oracle as
-the per-shard step (no GPU here), diagnostics all-reduced; the merged state must
-equal the single-process step bitwise and the diagnostics must match."""
+"""N>1 path on CPU: world_size-2 gloo process group, the product's shard plan
+(fsbm_decompose: i-slabs and WRF j-patches), the oracle as the per-shard step (no GPU
+here), diagnostics all-reduced by shard.reduce_diagnostics; the merged state must equal
+the single-process step bitwise and the diagnostics must match.  The device path of the
+same plan (fsbm_group_step_*) is tested on the GPU in tests/test_gpu_group.py."""
 import os
 import socket
 
@@ -33,31 +35,40 @@ def _problem(oracle):
     return grid, tabs, T, P, mask, B
 
 
-def _run_shard(oracle, grid, tabs, P, mask, B, i0, i1):
-    per_i = NK * NJ
-    sl = slice(i0 * per_i, i1 * per_i)
-    Bs = np.ascontiguousarray(B[:, sl])
+def _shard_index(r):
+    """Flat indices (reference layout of the full grid) of shard r's points, in the
+    reference layout of the shard itself."""
+    i = np.arange(r.ids - 1, r.ide)[:, None, None]
+    k = np.arange(NK)[None, :, None]
+    j = np.arange(r.jds - 1, r.jde)[None, None, :]
+    return ((i * NK + k) * NJ + j).reshape(-1)
+
+
+def _run_shard(oracle, grid, tabs, P, mask, B, r):
+    idx = _shard_index(r)
+    Bs = np.ascontiguousarray(B[:, idx])
     abd = oracle.default_registry()
     g = oracle.gain_table(grid.x, grid.ratio)
     x = grid.x
     m0 = float((Bs * x).sum())
-    st, cnt, err = oracle.step_grid(i1 - i0, NK, NJ, x, abd, tabs.t750.reshape(-1).copy(),
+    st, cnt, err = oracle.step_grid(r.ni(), NK, r.nj(), x, abd, tabs.t750.reshape(-1).copy(),
                                     tabs.t500.reshape(-1).copy(), g,
-                                    np.ascontiguousarray(mask[sl]), np.ascontiguousarray(P[sl]), Bs)
+                                    np.ascontiguousarray(mask[idx]), np.ascontiguousarray(P[idx]), Bs)
     assert st == 0
     d = shard.StepDiagnostics(int(cnt[0]), int(cnt[1]), int(cnt[2]), m0, float((Bs * x).sum()),
                               0.0, 0.0, -1)
     return Bs, d
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, split):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import pyoracle
+    from paper_2409_07232_b200 import Ranges
     O = pyoracle.Oracle()
     grid, tabs, T, P, mask, B = _problem(O)
-    i0, i1 = shard.slab(NI, world, rank)
-    Bs, d = _run_shard(O, grid, tabs, P, mask, B, i0, i1)
+    r = shard.decompose_shards(Ranges(1, NI, 1, NK, 1, NJ), world, split)[rank]
+    Bs, d = _run_shard(O, grid, tabs, P, mask, B, r)
     tot = shard.reduce_diagnostics(d, dist)
     np.save(os.path.join(out, f"shard{rank}.npy"), Bs)
     if rank == 0:
@@ -78,12 +89,17 @@ def test_slab_partition():
         shard.slab(3, 4, 0)
 
 
-def test_two_rank_gloo_equals_single(tmp_path, oracle):
+@pytest.mark.parametrize("split", ["i", "j"])
+def test_two_rank_gloo_equals_single(tmp_path, oracle, split):
+    from paper_2409_07232_b200 import Ranges
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), split), nprocs=world, join=True)
     grid, tabs, T, P, mask, B = _problem(oracle)
-    Bfull, dfull = _run_shard(oracle, grid, tabs, P, mask, B, 0, NI)
-    merged = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)], axis=1)
+    full = Ranges(1, NI, 1, NK, 1, NJ)
+    Bfull, dfull = _run_shard(oracle, grid, tabs, P, mask, B, full)
+    merged = np.zeros_like(Bfull)
+    for rk, r in enumerate(shard.decompose_shards(full, world, split)):
+        merged[:, _shard_index(r)] = np.load(tmp_path / f"shard{rk}.npy")
     assert np.array_equal(merged, Bfull)  # sharding never changes a point's result
     diag = np.load(tmp_path / "diag.npy")
     assert list(diag[:3].astype(np.int64)) == [dfull.triples, dfull.points, dfull.kernel_evals]
