@@ -299,13 +299,14 @@ def fp64_peak(dev_index):
 
 def ncu_traffic(nkr, points, tag=None):
     """DRAM bytes of the coal kernel per launch from a committed ncu --set full capture."""
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["by_nkr"]
+    for name in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):  # newest capture first
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", name)))["by_nkr"]
+        except Exception:
+            continue
         e = tr.get(tag or str(nkr))
         if e:
             return e["bytes_per_update"] * points, e["source"]
-    except Exception:
-        pass
     return None, None
 
 

@@ -231,13 +231,15 @@ def test_device_stale_mask_raises():
 
 def test_stiffness_message_carries_the_value(reference):
     """StiffnessError text as coalescence.cpp:319-325 ('would become negative (V)') plus
-    at_point's coordinates; the value matches the reference's to the printed digits."""
+    at_point's coordinates, identical to the reference's message in EXACT numerics."""
     nkr = 33
     grid = fsbm.make_mass_grid(nkr)
     tabs = fsbm.build_tables(grid, fsbm.default_pair_registry(),
                              fsbm.KernelParams("golovin", 1500.0, 1.5, 0.0))
     ctx = fsbm.CoalContext(grid, tabs)
-    T, P, B = reference.synthetic_case(3, 4, 5, 1.0, 11, nkr)
+    st0, _ = synth.thunderstorm_device(ctx, 3, 4, 5, 0.5, 11)
+    B = bins_np(st0, nkr)
+    T, P = st0.temperature.cpu().numpy(), st0.pressure.cpu().numpy()
     ref = B.copy()
     st_ref, _, _, err_ref = reference.fissioned_step(3, 4, 5, nkr, tabs.t750.reshape(-1).copy(),
                                                      tabs.t500.reshape(-1).copy(), T, P, ref,
@@ -252,6 +254,7 @@ def test_stiffness_message_carries_the_value(reference):
             fsbm.fissioned_step(st, None, fsbm.StepContext(ctx), fsbm.ExecPlan(numerics=numerics))
         e = ei.value
         assert e.point == tuple(int(v) for v in err_ref[2:5])
+        assert (e.category, e.bin) == (int(err_ref[0]), int(err_ref[1]))
         assert "would become negative (" in str(e) and e.value < 0
         if numerics == "exact":
             assert str(e) == ref_msg
