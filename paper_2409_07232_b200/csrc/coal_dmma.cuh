@@ -51,15 +51,12 @@
 
 namespace fsbm {
 
-// Deltas live in TMEM (tcgen05.ld/st) unless built with -DFSBM_DMMA_NO_TMEM (A/B): the 48
-// registers they free let the CTA run 4 point groups (16 warps x 128 registers) instead of
-// 3 (12 x 168) -- measured 96.0 vs 79.9 M upd/s at C2.
-#ifndef FSBM_DMMA_NO_TMEM
-#define FSBM_DMMA_TMEM 1
-#endif
+// Deltas live in TMEM (tcgen05.ld/st): the 48 registers they free let the CTA run 4 point
+// groups (16 warps x 128 registers) instead of 3 (12 x 168) -- measured 96.0 vs 79.9 M upd/s
+// at C2 in round 1 (the register variant is retired).
 
 constexpr int kDmmaRB = 4;   // full 8-row blocks handled by this kernel (nkr = 32 or 33)
-constexpr int kDmmaNBUF = 3; // per-pair table buffers in flight (TMA lookahead)
+constexpr int kDmmaNBUF = 2; // per-pair table buffers in flight per half (TMA lookahead)
 
 struct DmmaTables {
     int nkr = 0, S = 0, npairs = 0;
@@ -306,13 +303,13 @@ struct DmmaArgs {
 };
 
 constexpr int kDmmaNT = 2;                          // 8-point N-tiles per warp
-#ifdef FSBM_DMMA_TMEM // deltas in TMEM: 4 point groups (16 warps x 128 registers)
-constexpr int kDmmaG = 4;
-#else
-constexpr int kDmmaG = 3;                           // point groups per CTA
-#endif
-constexpr int kDmmaNP = kDmmaG * kDmmaNT * 8;       // 48 points per batch
-constexpr int kDmmaThreads = kDmmaG * kDmmaRB * 32; // 512 (TMEM) / 384
+constexpr int kDmmaG = 4;                           // point groups per CTA (16 points each)
+constexpr int kDmmaH = 2;                           // independent halves per CTA
+constexpr int kDmmaGH = kDmmaG / kDmmaH;            // point groups per half
+constexpr int kDmmaNP = kDmmaG * kDmmaNT * 8;       // 64 points in the CTA's work buffer
+constexpr int kDmmaNPH = kDmmaNP / kDmmaH;          // 32 points per half-batch
+constexpr int kDmmaThreads = kDmmaG * kDmmaRB * 32; // 512
+constexpr int kDmmaHT = kDmmaThreads / kDmmaH;      // 256 threads (8 warps) per half
 constexpr int kDmmaQP = (kDmmaNP + 15) / 16 * 16 + 4; // point pitch, = 4 mod 16: conflict-free B fragments
 
 /// register delta add with a runtime (warp-uniform) category
@@ -480,9 +477,14 @@ __device__ __forceinline__ void emit_switch(int sel, double (&D)[kNCat][kDmmaNT]
 #undef FSBM_EMIT_CASE
 }
 
+/// Named barrier over one half of the CTA (ids 1, 2; id 0 is __syncthreads).
+__device__ __forceinline__ void half_sync(int h) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(kDmmaHT) : "memory");
+}
+
 template <int NKRC>
 __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, DmmaArgs F) {
-    constexpr int NT = kDmmaNT, NP = kDmmaNP, RB = kDmmaRB;
+    constexpr int NT = kDmmaNT, NP = kDmmaNP, RB = kDmmaRB, NPH = kDmmaNPH, HT = kDmmaHT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // NKRC == 33: the headline grid with its extents compiled in (S = 36, one tail row)
     const int nkr = NKRC ? NKRC : A.nkr, S = NKRC ? (NKRC + 3) / 4 * 4 : F.S, TAIL = NKRC ? NKRC % 8 : F.tail;
@@ -490,18 +492,21 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const int KS = S / 4;
     const size_t TBL = static_cast<size_t>(S) * S;
     constexpr int NBUF = kDmmaNBUF;
-    double *tabs = reinterpret_cast<double *>(smem_raw);                 // [NBUF][T500|Kd][S][S]
-    double *gains = tabs + 2 * NBUF * TBL;                                 // [lo|hi][S][S]
+    // Two independent halves (8 warps, point groups {0,1} and {2,3}) share the CTA's
+    // shared memory but nothing else: each steps its own 32-point half-batches with its
+    // own table ring and named barrier, so one half's load / apply / stiffness /
+    // write-back phases overlap the other half's DMMA K-loops.
+    double *tabs = reinterpret_cast<double *>(smem_raw);                 // [H][NBUF][T500|Kd][S][S]
+    double *gains = tabs + 2 * kDmmaH * NBUF * TBL;                        // [lo|hi][S][S]
     double *work = gains + 2 * TBL;                                        // [6][S][QP]
-    double *carry = work + static_cast<size_t>(kNCat) * S * QP;            // [6][RB][NP]
-    double *tdel = carry + static_cast<size_t>(kNCat) * RB * NP;           // [6][NP]
+    double *tdel = work + static_cast<size_t>(kNCat) * S * QP;             // [6][NP]
     double *wts = tdel + static_cast<size_t>(kNCat) * NP;                  // [NP]
     unsigned long long *act = reinterpret_cast<unsigned long long *>(wts + NP);
     unsigned long long *ptrip = act + NP;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);             // [NBUF tables, gains]
-    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + NBUF + 1);        // [NP]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(ptrip + NP);             // [H][NBUF tables], gains
+    uint32_t *pidx = reinterpret_cast<uint32_t *>(mbar + kDmmaH * NBUF + 1); // [NP]
     int *pfail = reinterpret_cast<int *>(pidx + NP);                       // [NP]
-    __shared__ unsigned long long cta_act;
+    __shared__ unsigned long long cta_act[kDmmaH];
     // per point group and category: last bin holding a non-zero value at any live point.
     // Products with an exactly-zero spectrum value vanish (the reference skips rate == 0
     // triples, coalescence.cpp:286-292): a pass whose owner rows are all zero, or whose
@@ -509,16 +514,18 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     // the streamed spectrum's last non-zero bin.  (Cutting K-steps inside the unrolled
     // loops measured slower: the early exits break the schedule.)
     __shared__ int kzg[kDmmaG][kNCat];
-    __shared__ int relcnt[kDmmaNBUF];
+    __shared__ int relcnt[kDmmaH][kDmmaNBUF];
     __shared__ short ltop[kNCat * kDmmaNP];
 
-    const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
+    const int tid = threadIdx.x;
     const int wid = tid >> 5, lane = tid & 31;
-    // block b of group g, rotated by g so every SMSP (wid % 4) hosts a mix of blocks
-    // block rotated by group so every SMSP (wid % 4) hosts three different blocks: measured
-    // better than one block per SMSP (instruction-cache friendly, unbalanced) or the pairing
-    // {s, 3-s} per SMSP
+    // block b of group g, rotated by g so every SMSP (wid % 4) hosts all four blocks
+    // (instruction-cache friendly; the per-block K-loop costs 26/30/34/38 DMMAs balance
+    // per SMSP)
     const int g = wid / RB, b = (wid % RB + g) % RB;
+    const int h = g / kDmmaGH;                 // this warp's half
+    const int htid = tid - h * HT, hwid = htid >> 5, NWH = HT >> 5;
+    const int q0 = h * NPH;                    // the half's first point slot
     const int o0 = 8 * b;
     const int lr = lane >> 2, lc = lane & 3;
     const int qg = g * NT * 8;
@@ -531,16 +538,17 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     const double dt = A.dt_sub;
     const uint32_t tbytes = static_cast<uint32_t>(2 * TBL * sizeof(double));
     unsigned long long tr_acc = 0, pt_acc = 0, ev_acc = 0;
+    double *htabs = tabs + static_cast<size_t>(h) * NBUF * 2 * TBL;
+    uint64_t *hbar = mbar + h * NBUF, *gbar = mbar + kDmmaH * NBUF;
 
     auto W = [&](int c, int s, int q) -> double & {
         return work[(static_cast<size_t>(c) * S + s) * QP + q];
     };
 
     if (tid == 0) {
-        for (int i = 0; i <= NBUF; ++i) mbar_init(&mbar[i], 1);
+        for (int i = 0; i <= kDmmaH * NBUF; ++i) mbar_init(&mbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-#ifdef FSBM_DMMA_TMEM
     __shared__ uint32_t tmem_base;
     if (wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
@@ -551,21 +559,20 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     tm_fence_after();
     // this warp's slot: lanes 32*(wid%4).., columns (wid/4)*96: [0,48) deltas, [48,96) carries
     const uint32_t tmw = tmem_base + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + (wid >> 2) * 96;
-#else
-    __syncthreads();
-#endif
     if (tid == 0) { // pair-independent gain coefficients, once per CTA
-        mbar_expect_tx(&mbar[NBUF], static_cast<uint32_t>(2 * TBL * sizeof(double)));
-        tma_bulk_g2s(gains, F.gains, static_cast<uint32_t>(2 * TBL * sizeof(double)), &mbar[NBUF]);
+        mbar_expect_tx(gbar, static_cast<uint32_t>(2 * TBL * sizeof(double)));
+        tma_bulk_g2s(gains, F.gains, static_cast<uint32_t>(2 * TBL * sizeof(double)), gbar);
     }
-    uint32_t pbase = 0; // pairs processed so far: pair #m uses buffer m % NBUF, phase (m / NBUF) & 1
+    uint32_t pbase = 0; // pairs processed so far by this half: pair #m uses buffer m % NBUF,
+                        // phase (m / NBUF) & 1
     bool gains_ready = false;
     PROF_DECL
 
-    for (uint32_t batch = blockIdx.x; batch < F.nbatches && batch * static_cast<uint32_t>(NP) < nact;
-         batch += gridDim.x) {
-        for (int q = tid; q < NP; q += nthr) {
-            const uint32_t idx = batch * static_cast<uint32_t>(NP) + q;
+    for (uint32_t hb = kDmmaH * blockIdx.x + h; hb < F.nbatches && hb * static_cast<uint32_t>(NPH) < nact;
+         hb += kDmmaH * gridDim.x) {
+        if (htid < NPH) {
+            const int q = q0 + htid;
+            const uint32_t idx = hb * static_cast<uint32_t>(NPH) + htid;
             const bool live = idx < nact;
             const uint32_t p = live ? A.active[idx] : 0xffffffffu;
             pidx[q] = p;
@@ -573,13 +580,13 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             pfail[q] = live ? 0 : 1;
             ptrip[q] = 0;
         }
-        __syncthreads();
+        half_sync(h);
         { // spectra -> work, coalesced: a warp instruction covers 4 points x 8 consecutive bins
           // (64-byte runs of each point's spectrum); quads of (category, 4 points) per warp
-            constexpr int NQ = kNCat * NP / 4; // 72 quads
+            constexpr int NQ = kNCat * NPH / 4; // 48 quads per half
             const int qs = lane >> 3, kc = lane & 7;
-            for (int u = wid; u < NQ; u += NW) {
-                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+            for (int u = hwid; u < NQ; u += NWH) {
+                const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
                 const uint32_t p = pidx[q];
                 const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
                 double v[5];
@@ -601,17 +608,18 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             }
         }
         if (!gains_ready) {
-            mbar_wait(&mbar[NBUF], 0);
+            mbar_wait(gbar, 0);
             gains_ready = true;
         }
-        __syncthreads();
+        half_sync(h);
 
         for (int sub = 0; sub < A.substeps; ++sub) {
-            if (tid == 0) cta_act = 0ull;
-            for (int f = tid; f < kNCat * (RB + 1) * NP; f += nthr) carry[f] = 0.0; // carry + tdel
-            if (tid < kDmmaG * kNCat) kzg[tid / kNCat][tid % kNCat] = -1;
-            __syncthreads();
-            for (int q = tid; q < NP; q += nthr) { // all_zero (coalescence.cpp:270-273)
+            if (htid == 0) cta_act[h] = 0ull;
+            for (int f = htid; f < kNCat * NPH; f += HT) tdel[(f / NPH) * NP + q0 + f % NPH] = 0.0;
+            if (htid < kDmmaGH * kNCat) kzg[h * kDmmaGH + htid / kNCat][htid % kNCat] = -1;
+            half_sync(h);
+            if (htid < NPH) { // all_zero (coalescence.cpp:270-273)
+                const int q = q0 + htid;
                 unsigned nz = 0;
                 for (int c = 0; c < kNCat; ++c) { // last non-zero bin (the load found it for sub 0)
                     int l = ltop[c * NP + q];
@@ -630,32 +638,24 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     }
                 if (pfail[q] == 0) {
                     act[q] = m;
-                    atomicOr(&cta_act, m);
+                    atomicOr(&cta_act[h], m);
                     ptrip[q] += trip;
                 } else {
                     act[q] = 0;
                 }
             }
-            __syncthreads();
-            const unsigned long long amask = cta_act;
+            half_sync(h);
+            const unsigned long long amask = cta_act[h];
 
             PROF_MARK(0)
-#ifdef FSBM_DMMA_TMEM
             {
                 const double z[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int c = 0; c < 2 * kNCat; ++c) tm_st4_nowait(tmw + 8 * c, z); // deltas, carries
                 tm_wait_st();
             }
-#else
-            double D[kNCat][NT][2];
-#pragma unroll
-            for (int c = 0; c < kNCat; ++c)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) D[c][nt][0] = D[c][nt][1] = 0.0;
-#endif
 
-            // Pair pipeline without CTA barriers (see header).
+            // Pair pipeline without barriers (see header), one ring per half.
             auto next_pair = [&](int p) -> int {
                 if (p < 0) return -1;
                 const unsigned long long rest = amask & ~((2ull << p) - 1ull);
@@ -663,33 +663,32 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             };
             int cur = amask ? __ffsll(static_cast<long long>(amask)) - 1 : -1;
             int n = 0;
-            if (tid == 0) { // prime all buffers with the first NBUF active pairs
+            if (htid == 0) { // prime all buffers with the first NBUF active pairs
                 fence_proxy_async();
                 int pp = cur;
                 for (int i = 0; i < NBUF; ++i, pp = next_pair(pp)) {
                     const int bi = (pbase + i) % NBUF;
-                    relcnt[bi] = 0;
+                    relcnt[h][bi] = 0;
                     if (pp >= 0) {
-                        mbar_expect_tx(&mbar[bi], tbytes);
-                        tma_bulk_g2s(tabs + bi * 2 * TBL, F.blob + static_cast<size_t>(pp) * 2 * TBL, tbytes,
-                                     &mbar[bi]);
+                        mbar_expect_tx(&hbar[bi], tbytes);
+                        tma_bulk_g2s(htabs + bi * 2 * TBL, F.blob + static_cast<size_t>(pp) * 2 * TBL, tbytes,
+                                     &hbar[bi]);
                     }
                 }
             }
-            __syncthreads();
+            half_sync(h);
             while (cur >= 0) {
                 const uint32_t m = pbase + n;
                 const int buf = m % NBUF;
                 const int nxt = next_pair(cur);
                 PROF_MARK(7)
-                mbar_wait(&mbar[buf], (m / NBUF) & 1u);
+                mbar_wait(&hbar[buf], (m / NBUF) & 1u);
                 PROF_MARK(2)
-                const double *T5 = tabs + buf * 2 * TBL;
+                const double *T5 = htabs + buf * 2 * TBL;
                 const double *Td = T5 + TBL;
                 const double *Glo = gains, *Ghi = gains + TBL;
                 const int pa = A.pairs.a[cur], pb = A.pairs.b[cur], pd = A.pairs.d[cur];
                 const bool self = pa == pb;
-
                 bool on[NT][2];
                 double we[NT][2];
                 const double wu = wts[qg]; // first point of the warp's group
@@ -835,9 +834,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     PROF_MARK(3)
                     // emission: rows o, points qg+nt*8+2lc+e; hi-gain -> row o+1
                     DmmaAcc L, Gn;
-#ifdef FSBM_DMMA_TMEM
                     DmmaAcc Cy;
-#endif
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -848,13 +845,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             const double up = __shfl_up_sync(0xffffffffu, y3, 4);
                             L[nt][e] = f * Y1[nt][e];
                             Gn[nt][e] = lr > 0 ? fma(f, Y2[nt][e], up) : f * Y2[nt][e];
-#ifdef FSBM_DMMA_TMEM
                             Cy[nt][e] = lr == 7 ? y3 : 0.0; // hi gain of row 7 -> next block head
-#else
-                            if (lr == 7) carry[(static_cast<size_t>(pd) * RB + b) * NP + q] += y3;
-#endif
                         }
-#ifdef FSBM_DMMA_TMEM
                     {
                         const uint32_t tf = tmw + 8 * fcat, tp = tmw + 8 * pd, tcy = tmw + 48 + 8 * pd;
                         double d[4], e4[4], cy[4];
@@ -880,9 +872,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             tm_st4_nowait(tp, e4);
                         }
                     }
-#else
-                    emit_switch(fcat * kNCat + pd, D, L, Gn);
-#endif
 
                     PROF_MARK(6)
                     } // non-zero block
@@ -918,9 +907,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 // exception cells (non owner-local targets), gathered by the target's owner
                 if (!NKRC && F.nexc > 0) { // (the compiled-in 33-bin grid has none)
                     for (int kind = self ? 1 : 0; kind <= (self ? 1 : 2); kind += self ? 1 : 2) {
-#ifdef FSBM_DMMA_TMEM
                         double exd[4] = {0.0, 0.0, 0.0, 0.0};
-#endif
                         const int T = o0 + lr;
                         const int e0 = __ldg(F.exc_off + kind * (nkr + 1) + T);
                         const int e1 = __ldg(F.exc_off + kind * (nkr + 1) + T + 1);
@@ -934,14 +921,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                                 for (int e = 0; e < 2; ++e) {
                                     const int q = qg + nt * 8 + 2 * lc + e;
                                     const double x = fma(we[nt][e], kd, k5) * W(pa, en.i, q) * W(pb, en.j, q);
-#ifdef FSBM_DMMA_TMEM
                                     if (on[nt][e]) exd[2 * nt + e] += en.coef * x;
-#else
-                                    if (on[nt][e]) dadd_cat(D, pd, nt, e, en.coef * x);
-#endif
                                 }
                         }
-#ifdef FSBM_DMMA_TMEM
                         if (__any_sync(0xffffffffu, e1 > e0)) {
                             double d[4];
                             tm_wait_st();
@@ -955,7 +937,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                             tm_st4_nowait(tmw + 8 * pd, d);
                             tm_wait_st();
                         }
-#endif
                         if (TAIL > 0 && (lane & 7) == 0) { // targets in the top row: the scalar
                             const int qt = qg + 4 * b + (lane >> 3); // top row's point split
                             const int e2 = __ldg(F.exc_off + kind * (nkr + 1) + ot);
@@ -970,21 +951,21 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         }
                     }
                 }
-                // release buffer `buf`; the last warp out refills it with pair n+2
+                // release buffer `buf`; the last warp of the half refills it with pair n+NBUF
                 __syncwarp();
                 if (lane == 0) {
                     __threadfence_block();
-                    const int old = atomicAdd(&relcnt[buf], 1);
-                    if (old == NW - 1) {
-                        relcnt[buf] = 0;
+                    const int old = atomicAdd(&relcnt[h][buf], 1);
+                    if (old == NWH - 1) {
+                        relcnt[h][buf] = 0;
                         __threadfence_block();
                         int p2 = nxt; // pair n + NBUF
                         for (int i = 1; i < NBUF; ++i) p2 = next_pair(p2);
                         if (p2 >= 0) {
                             fence_proxy_async();
-                            mbar_expect_tx(&mbar[buf], tbytes);
-                            tma_bulk_g2s(tabs + buf * 2 * TBL, F.blob + static_cast<size_t>(p2) * 2 * TBL,
-                                         tbytes, &mbar[buf]);
+                            mbar_expect_tx(&hbar[buf], tbytes);
+                            tma_bulk_g2s(htabs + buf * 2 * TBL, F.blob + static_cast<size_t>(p2) * 2 * TBL,
+                                         tbytes, &hbar[buf]);
                         }
                     }
                 }
@@ -994,11 +975,10 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             pbase += n;
             PROF_MARK(7)
             // ---- Jacobi apply (coalescence.cpp:313-328): every read of `work` for this
-            // substep is done, so owners add their register deltas in place, then the
-            // cross-block carries and the top row, then the stiffness scan.
-            __syncthreads();
+            // substep (in this half) is done, so owners add their TMEM deltas in place, then
+            // the cross-block carries and the top row, then the stiffness scan.
+            half_sync(h);
             PROF_MARK(4)
-#ifdef FSBM_DMMA_TMEM
             tm_wait_st();
 #pragma unroll
             for (int c = 0; c < kNCat; ++c) {
@@ -1011,19 +991,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     W(c, o0 + lr, q) = fma(dt, d[i], W(c, o0 + lr, q));
                 }
             }
-#else
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int q = qg + nt * 8 + 2 * lc + e;
-                    const int o = o0 + lr;
-#pragma unroll
-                    for (int c = 0; c < kNCat; ++c) W(c, o, q) = fma(dt, D[c][nt][e], W(c, o, q));
-                }
-#endif
-            __syncthreads();
-#ifdef FSBM_DMMA_TMEM
+            half_sync(h);
             // block-head carries from TMEM (lane row 7 holds them); the last block's go to
             // the top row through tdel
 #pragma unroll
@@ -1040,43 +1008,32 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     }
                 }
             }
-            __syncthreads();
+            half_sync(h);
             if (TAIL > 0)
-                for (int c = 0; c < kNCat; ++c)
-                    for (int q = tid; q < NP; q += nthr)
-                        W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q], W(c, ot, q));
-#else
-            for (int c = 0; c < kNCat; ++c) // carries into block heads and the top row
-                for (int q = tid; q < NP; q += nthr) {
-                    for (int bb = 1; bb < RB; ++bb)
-                        W(c, 8 * bb, q) = fma(dt, carry[(static_cast<size_t>(c) * RB + bb - 1) * NP + q], W(c, 8 * bb, q));
-                    if (TAIL > 0)
-                        W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q] +
-                                                  carry[(static_cast<size_t>(c) * RB + RB - 1) * NP + q],
-                                          W(c, ot, q));
+                for (int f = htid; f < kNCat * NPH; f += HT) {
+                    const int c = f / NPH, q = q0 + f % NPH;
+                    W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q], W(c, ot, q));
                 }
-#endif
-            __syncthreads();
+            half_sync(h);
             for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
-                for (int k = wid; k < nkr; k += NW)
-                    for (int q = lane; q < NP; q += 32) {
-                        const uint32_t p = pidx[q];
-                        if (p == 0xffffffffu || pfail[q] != 0) continue;
-                        if (W(c, k, q) < 0.0) {
-                            report_stiffness(A, p, c, k, W(c, k, q));
-                            pfail[q] = 2;
-                        }
+                for (int k = hwid; k < nkr; k += NWH) {
+                    const int q = q0 + lane; // NPH == 32: one point per lane
+                    const uint32_t p = pidx[q];
+                    if (p == 0xffffffffu || pfail[q] != 0) continue;
+                    if (W(c, k, q) < 0.0) {
+                        report_stiffness(A, p, c, k, W(c, k, q));
+                        pfail[q] = 2;
                     }
-            __syncthreads();
-            for (int q = tid; q < NP; q += nthr)
-                if (pfail[q] == 2) pfail[q] = 3;
+                }
+            half_sync(h);
+            if (htid < NPH && pfail[q0 + htid] == 2) pfail[q0 + htid] = 3;
         }
         // ---- write back + counters ----
         {
-            constexpr int NQ = kNCat * NP / 4;
+            constexpr int NQ = kNCat * NPH / 4;
             const int qs = lane >> 3, kc = lane & 7;
-            for (int u = wid; u < NQ; u += NW) {
-                const int c = u / (NP / 4), q = 4 * (u % (NP / 4)) + qs;
+            for (int u = hwid; u < NQ; u += NWH) {
+                const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
                 const uint32_t p = pidx[q];
                 if (p == 0xffffffffu) continue;
                 double *dst = A.bins[c] + static_cast<size_t>(p) * nkr;
@@ -1087,24 +1044,24 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 }
             }
         }
-        for (int q = tid; q < NP; q += nthr) {
-            if (pidx[q] == 0xffffffffu || pfail[q] != 0) continue;
-            tr_acc += ptrip[q];
-            pt_acc += 1;
-            ev_acc += A.kernel_strategy ? ptrip[q] : full_evals;
+        if (htid < NPH) {
+            const int q = q0 + htid;
+            if (pidx[q] != 0xffffffffu && pfail[q] == 0) {
+                tr_acc += ptrip[q];
+                pt_acc += 1;
+                ev_acc += A.kernel_strategy ? ptrip[q] : full_evals;
+            }
         }
-        __syncthreads();
+        half_sync(h);
         PROF_MARK(5)
     }
     PROF_FLUSH
-#ifdef FSBM_DMMA_TMEM
     tm_fence_before();
     __syncthreads();
     if (wid == 0) {
         tm_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
-#endif
     for (int o = 16; o > 0; o >>= 1) {
         tr_acc += __shfl_down_sync(0xffffffffu, tr_acc, o);
         pt_acc += __shfl_down_sync(0xffffffffu, pt_acc, o);
@@ -1120,9 +1077,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
 inline size_t dmma_smem_bytes(int nkr, int S, int QP) {
     constexpr int NP = kDmmaNP;
     const size_t TBL = static_cast<size_t>(S) * S;
-    const size_t d = (2 * kDmmaNBUF + 2) * TBL + static_cast<size_t>(kNCat) * S * QP + static_cast<size_t>(kNCat) * kDmmaRB * NP +
+    const size_t d = (2 * kDmmaH * kDmmaNBUF + 2) * TBL + static_cast<size_t>(kNCat) * S * QP +
                      static_cast<size_t>(kNCat) * NP + NP;
-    return d * 8 + NP * 8 * 2 + (kDmmaNBUF + 1) * 8 + NP * 4 + NP * 4;
+    return d * 8 + NP * 8 * 2 + (kDmmaH * kDmmaNBUF + 1) * 8 + NP * 4 + NP * 4;
 }
 
 /// Returns -1 when this geometry cannot run the DMMA path (caller falls back).
@@ -1146,7 +1103,7 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
         for (int b = 0; b < kDmmaRB; ++b)
             F.std_classes = F.std_classes && T.kf[V][b] == 2 * b && T.km[V][b] == 2 * b + 2;
     if (const char *ev = std::getenv("FSBM_DMMA_UNROLL"); ev && ev[0] == '0') F.std_classes = 0; // A/B
-    F.nbatches = (A.nactive_host + kDmmaNP - 1) / kDmmaNP;
+    F.nbatches = (A.nactive_host + kDmmaNPH - 1) / kDmmaNPH; // 32-point half-batches
     F.blob = T.blob;
     F.gains = T.gains;
     F.exc_off = T.exc_off;
@@ -1159,7 +1116,7 @@ inline int launch_dmma(const DmmaTables &T, const FastTables & /*FT*/, const Ste
         fast_err() = "dmma path: cannot reserve shared memory";
         return 6;
     }
-    const int grid = static_cast<int>(std::min<uint32_t>(F.nbatches, num_sms));
+    const int grid = static_cast<int>(std::min<uint32_t>((F.nbatches + kDmmaH - 1) / kDmmaH, num_sms));
 #ifdef FSBM_DMMA_PROF
     constexpr int kPW = kDmmaThreads / 32; // warps per CTA
     static unsigned long long *dprof = nullptr;

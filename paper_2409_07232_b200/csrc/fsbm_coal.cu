@@ -20,7 +20,7 @@
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
-#include "../../include/fsbm_coal.h"
+#include "fsbm_coal.h"
 #include "coal_exact.cuh"
 #include "coal_fast.cuh"
 #include "coal_dmma.cuh"

@@ -6,4 +6,4 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 name=$1; src=$2; shift 2
 mkdir -p "$ROOT/build/ab"
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -shared \
-  --expt-relaxed-constexpr -I "$ROOT/include" "$@" "$src/fsbm_coal.cu" -o "$ROOT/build/ab/$name.so"
+  --expt-relaxed-constexpr -I "$ROOT/include" "$@" "$src/fsbm_coal.cu" -o "$ROOT/build/ab/$name.so" -ldl
