@@ -234,6 +234,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+/// 8-byte asynchronous global -> shared copy (LDGSTS: no register round trip).
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 /// D(8x8) += A(8x4) B(4x8), FP64 tensor core.
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -566,46 +573,66 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     uint32_t pbase = 0; // pairs processed so far by this half: pair #m uses buffer m % NBUF,
                         // phase (m / NBUF) & 1
     bool gains_ready = false;
+    // rows [nkr, S) of every category stay zero (K-step padding read by the B fragments)
+    for (int f = tid; f < kNCat * (S - nkr) * NP; f += kDmmaThreads) {
+        const int q = f % NP, r = f / NP;
+        W(r / (S - nkr), nkr + r % (S - nkr), q) = 0.0;
+    }
+    // the next half-batch's point index and pressure weight (lanes htid < NPH), loaded
+    // ahead during the previous half-batch's apply so the batch start does not wait on them
+    auto fetch_point = [&](uint32_t hbx, uint32_t &p, double &w) {
+        const uint32_t idx = hbx * static_cast<uint32_t>(NPH) + htid;
+        const bool live = hbx < F.nbatches && idx < nact;
+        p = live ? A.active[idx] : 0xffffffffu;
+        w = live ? pressure_weight(A.pressure[p]) : 0.0;
+    };
+    __shared__ uint32_t nx_p[kDmmaNP];
+    __shared__ double nx_w[kDmmaNP];
+    if (htid < NPH) fetch_point(kDmmaH * blockIdx.x + h, nx_p[q0 + htid], nx_w[q0 + htid]);
+    __syncthreads(); // the padding rows are zero for both halves
     PROF_DECL
 
     for (uint32_t hb = kDmmaH * blockIdx.x + h; hb < F.nbatches && hb * static_cast<uint32_t>(NPH) < nact;
          hb += kDmmaH * gridDim.x) {
         if (htid < NPH) {
             const int q = q0 + htid;
-            const uint32_t idx = hb * static_cast<uint32_t>(NPH) + htid;
-            const bool live = idx < nact;
-            const uint32_t p = live ? A.active[idx] : 0xffffffffu;
-            pidx[q] = p;
-            wts[q] = live ? pressure_weight(A.pressure[p]) : 0.0;
-            pfail[q] = live ? 0 : 1;
+            pidx[q] = nx_p[q];
+            wts[q] = nx_w[q];
+            pfail[q] = nx_p[q] != 0xffffffffu ? 0 : 1;
             ptrip[q] = 0;
         }
         half_sync(h);
-        { // spectra -> work, coalesced: a warp instruction covers 4 points x 8 consecutive bins
-          // (64-byte runs of each point's spectrum); quads of (category, 4 points) per warp
-            constexpr int NQ = kNCat * NPH / 4; // 48 quads per half
-            const int qs = lane >> 3, kc = lane & 7;
-            for (int u = hwid; u < NQ; u += NWH) {
-                const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
-                const uint32_t p = pidx[q];
-                const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
-                double v[5];
+        // spectra -> work by asynchronous copies (LDGSTS), all issued before one wait: a
+        // warp instruction covers 4 points x 8 consecutive bins (64-byte runs of each point's
+        // spectrum); quads of (category, 4 points) per warp
+        constexpr int NQ = kNCat * NPH / 4; // 48 quads per half
+        const int qs = lane >> 3, kc = lane & 7;
+        for (int u = hwid; u < NQ; u += NWH) {
+            const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
+            const uint32_t p = pidx[q];
+            const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
 #pragma unroll
-                for (int jj = 0; jj < 5; ++jj) {
-                    const int k = kc + 8 * jj;
-                    v[jj] = p != 0xffffffffu && k < nkr ? __ldg(src + k) : 0.0;
+            for (int jj = 0; jj < 5; ++jj) {
+                const int k = kc + 8 * jj;
+                if (k < nkr) {
+                    if (p != 0xffffffffu) cp_async8(&W(c, k, q), src + k);
+                    else W(c, k, q) = 0.0;
                 }
-                int top = -1; // last non-zero bin of this (category, point), for the first substep
-#pragma unroll
-                for (int jj = 0; jj < 5; ++jj) {
-                    const int k = kc + 8 * jj;
-                    if (k < S) W(c, k, q) = v[jj];
-                    if (v[jj] != 0.0) top = k;
-                }
-#pragma unroll
-                for (int d = 1; d < 8; d <<= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, d));
-                if (kc == 0) ltop[c * NP + q] = static_cast<short>(top);
             }
+        }
+        cp_async_wait_all();
+        half_sync(h);
+        for (int u = hwid; u < NQ; u += NWH) { // last non-zero bin per (category, point)
+            const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
+            int top = -1;
+#pragma unroll
+            for (int jj = 0; jj < 5; ++jj) {
+                const int k = kc + 8 * jj;
+                if (k < nkr && W(c, k, q) != 0.0) top = k;
+            }
+#pragma unroll
+            for (int d = 1; d < 8; d <<= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, d));
+            if (kc == 0) ltop[c * NP + q] = static_cast<short>(top);
         }
         if (!gains_ready) {
             mbar_wait(gbar, 0);
@@ -975,56 +1002,96 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             pbase += n;
             PROF_MARK(7)
             // ---- Jacobi apply (coalescence.cpp:313-328): every read of `work` for this
-            // substep (in this half) is done, so owners add their TMEM deltas in place, then
-            // the cross-block carries and the top row, then the stiffness scan.
+            // substep (in this half) is done.  Phase 1: each warp adds its TMEM deltas to its
+            // own 8 rows and parks the hi-gain carry of its row 7 (TMEM) for the next block's
+            // head in the half's idle table ring (block 3's goes to the top row via tdel).
+            // Phase 2: block heads take the carry, the top row takes tdel, and each warp checks
+            // the rows it owns for negative values (no clamping; every failing bin of a
+            // point is offered, the sink keeps the first in serial order).
             half_sync(h);
             PROF_MARK(4)
+            const bool prefetch = sub == A.substeps - 1 && htid < NPH;
+            uint32_t pf_p = 0xffffffffu; // the next half-batch's points, loaded early
+            double pf_w = 0.0;
+            if (prefetch) fetch_point(hb + kDmmaH * gridDim.x, pf_p, pf_w);
+            double *cscr = htabs; // [6][RB-1][NP] carry scratch (the ring is idle here)
+            double nv[kNCat][4];
             tm_wait_st();
+            {
+                double d[kNCat][4];
 #pragma unroll
-            for (int c = 0; c < kNCat; ++c) {
-                double d[4];
-                tm_ld4_nowait(tmw + 8 * c, d);
+                for (int c = 0; c < kNCat; ++c) tm_ld4_nowait(tmw + 8 * c, d[c]);
                 tm_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
-                    W(c, o0 + lr, q) = fma(dt, d[i], W(c, o0 + lr, q));
-                }
-            }
-            half_sync(h);
-            // block-head carries from TMEM (lane row 7 holds them); the last block's go to
-            // the top row through tdel
-#pragma unroll
-            for (int c = 0; c < kNCat; ++c) {
-                double cy[4];
-                tm_ld4_nowait(tmw + 48 + 8 * c, cy);
-                tm_wait_ld();
-                if (lr == 7) {
+                for (int c = 0; c < kNCat; ++c)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
-                        if (b + 1 < RB) W(c, 8 * (b + 1), q) = fma(dt, cy[i], W(c, 8 * (b + 1), q));
-                        else if (TAIL > 0) tdel[static_cast<size_t>(c) * NP + q] += cy[i];
+                        nv[c][i] = fma(dt, d[c][i], W(c, o0 + lr, q));
+                        W(c, o0 + lr, q) = nv[c][i];
                     }
+            }
+            {
+                double cy[kNCat][4];
+#pragma unroll
+                for (int c = 0; c < kNCat; ++c) tm_ld4_nowait(tmw + 48 + 8 * c, cy[c]);
+                tm_wait_ld();
+                if (lr == 7) {
+#pragma unroll
+                    for (int c = 0; c < kNCat; ++c)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
+                            if (b + 1 < RB) cscr[(static_cast<size_t>(c) * (RB - 1) + b) * NP + q] = cy[c][i];
+                            else if (TAIL > 0) tdel[static_cast<size_t>(c) * NP + q] += cy[c][i];
+                        }
                 }
             }
             half_sync(h);
-            if (TAIL > 0)
-                for (int f = htid; f < kNCat * NPH; f += HT) {
-                    const int c = f / NPH, q = q0 + f % NPH;
-                    W(c, ot, q) = fma(dt, tdel[static_cast<size_t>(c) * NP + q], W(c, ot, q));
-                }
-            half_sync(h);
-            for (int c = 0; c < kNCat; ++c) // stiffness: no clamping, report the first point
-                for (int k = hwid; k < nkr; k += NWH) {
-                    const int q = q0 + lane; // NPH == 32: one point per lane
+            if (b > 0 && lr == 0) { // block head: the previous block's carry
+#pragma unroll
+                for (int c = 0; c < kNCat; ++c)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
+                        nv[c][i] = fma(dt, cscr[(static_cast<size_t>(c) * (RB - 1) + b - 1) * NP + q], nv[c][i]);
+                        W(c, o0, q) = nv[c][i];
+                    }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { // the first failing category of each of the lane's points
+                int cf = -1;
+                double vf = 0.0;
+#pragma unroll
+                for (int c = kNCat - 1; c >= 0; --c)
+                    if (nv[c][i] < 0.0) {
+                        cf = c;
+                        vf = nv[c][i];
+                    }
+                if (cf >= 0) {
+                    const int q = qg + (i >> 1) * 8 + 2 * lc + (i & 1);
                     const uint32_t p = pidx[q];
-                    if (p == 0xffffffffu || pfail[q] != 0) continue;
-                    if (W(c, k, q) < 0.0) {
-                        report_stiffness(A, p, c, k, W(c, k, q));
+                    if (p != 0xffffffffu && (pfail[q] & 1) == 0) {
+                        report_stiffness(A, p, cf, o0 + lr, vf);
                         pfail[q] = 2;
                     }
                 }
+            }
+            if (TAIL > 0 && b == RB - 1) // the top row of this group's 16 points
+                for (int f = lane; f < kNCat * NT * 8; f += 32) {
+                    const int c = f / (NT * 8), q = qg + f % (NT * 8);
+                    const double v = fma(dt, tdel[static_cast<size_t>(c) * NP + q], W(c, ot, q));
+                    W(c, ot, q) = v;
+                    const uint32_t p = pidx[q];
+                    if (v < 0.0 && p != 0xffffffffu && (pfail[q] & 1) == 0) {
+                        report_stiffness(A, p, c, ot, v);
+                        pfail[q] = 2;
+                    }
+                }
+            if (prefetch) {
+                nx_p[q0 + htid] = pf_p;
+                nx_w[q0 + htid] = pf_w;
+            }
             half_sync(h);
             if (htid < NPH && pfail[q0 + htid] == 2) pfail[q0 + htid] = 3;
         }
