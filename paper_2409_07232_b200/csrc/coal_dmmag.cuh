@@ -293,6 +293,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     __shared__ int qcnt[4];
     __shared__ int npass;
     __shared__ uint32_t tmem_base;
+#ifdef FSBM_SYNCCHECK_MBAR
+    // compute-sanitizer synccheck (CUDA 12.9) aborts a tcgen05 kernel that initialises no
+    // mbarrier ("Missing init" at shared 0x0); its build variant adds one unused barrier
+    __shared__ uint64_t synccheck_bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&synccheck_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+#endif
     __shared__ unsigned long long cnt_sh[3];
 
     const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
