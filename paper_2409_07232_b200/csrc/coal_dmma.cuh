@@ -523,6 +523,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     __shared__ int kzg[kDmmaG][kNCat];
     __shared__ int relcnt[kDmmaH][kDmmaNBUF];
     __shared__ short ltop[kNCat * kDmmaNP];
+    __shared__ unsigned char nzq[kDmmaNP];
+    __shared__ unsigned char wmode_s[kDmmaThreads / 32];
 
     const int tid = threadIdx.x;
     const int wid = tid >> 5, lane = tid & 31;
@@ -621,6 +623,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
             }
         }
         cp_async_wait_all();
+        // pressure-weight mode of the warp's 16 points, once per half-batch (see the pair loop)
+        {
+            const double w0 = wts[qg], wl = wts[qg + (lane & 15)];
+            const int wm = __all_sync(0xffffffffu, wl == 0.0) ? 0 : __all_sync(0xffffffffu, wl == w0) ? 1 : 2;
+            if (lane == 0) wmode_s[wid] = static_cast<unsigned char>(wm);
+        }
         half_sync(h);
         for (int u = hwid; u < NQ; u += NWH) { // last non-zero bin per (category, point)
             const int c = u / (NPH / 4), q = q0 + 4 * (u % (NPH / 4)) + qs;
@@ -670,9 +678,15 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 } else {
                     act[q] = 0;
                 }
+                nzq[q] = pfail[q] == 0 ? static_cast<unsigned char>(nz) : 0;
             }
             half_sync(h);
             const unsigned long long amask = cta_act[h];
+            // the non-zero-category bits of this lane's four points, 6 bits each: pair p is
+            // active at point i iff bit 6i + a[p] is set (coalescence.cpp:270-273)
+            uint32_t lnz = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) lnz |= static_cast<uint32_t>(nzq[qg + (i >> 1) * 8 + 2 * lc + (i & 1)]) << (6 * i);
 
             PROF_MARK(0)
             {
@@ -719,24 +733,20 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                 bool on[NT][2];
                 double we[NT][2];
                 const double wu = wts[qg]; // first point of the warp's group
-                bool all0 = true, allu = true;
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const int q = qg + nt * 8 + 2 * lc + e;
-                        on[nt][e] = act[q] >> cur & 1ull;
-                        we[nt][e] = wts[q];
-                        all0 = all0 && we[nt][e] == 0.0;
-                        allu = allu && we[nt][e] == wu;
+                        on[nt][e] = lnz >> (6 * (2 * nt + e) + pa) & 1u;
+                        we[nt][e] = NKRC ? 0.0 : wts[qg + nt * 8 + 2 * lc + e]; // generic paths only
                     }
-                // Pressure-weight mode of the warp's 16 points (warp-uniform).  Points are
-                // compacted in GridState order (j fastest), so a group of 16 almost always
-                // sits on one model level and shares one pressure:
+                // Pressure-weight mode of the warp's 16 points (warp-uniform, set once per
+                // half-batch).  Points are compacted in GridState order (j fastest), so a group
+                // of 16 almost always sits on one model level and shares one pressure:
                 //   0: all w == 0 (p <= 500 hPa): K500 + Kd*0 == K500 exactly -> one half
                 //   1: all w == wu: K = K500 + wu*Kd interpolated in the A fragment -> one half
                 //   2: otherwise (group straddles a level): K500 half + w * (Kd half)
-                const int wmode = __all_sync(0xffffffffu, all0) ? 0 : __all_sync(0xffffffffu, allu) ? 1 : 2;
+                const int wmode = wmode_s[wid];
                 const double *vbase[2] = {&W(pb, lc, qg + lr), &W(pa, lc, qg + lr)};
 
                 for (int X = 0; X < (self ? 1 : 2); ++X) {
@@ -910,13 +920,31 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         const double wq = wts[qt];
                         const double *vt = &W(X == 0 ? pb : pa, 0, qt);
                         double y1 = 0.0, y2 = 0.0;
-                        for (int sx = sc0; sx <= kzs; sx += 8) {
-                            const int ti = X == 0 ? ot * S + sx : sx * S + ot;
-                            const double m = V == 2 ? (sx <= ot ? 1.0 : 0.0)
-                                                    : (sx < ot ? 1.0 : (V == 1 && sx == ot ? 0.5 : 0.0));
-                            const double kv = fma(wq, Td[ti], T5[ti]) * vt[static_cast<size_t>(sx) * QP];
-                            y1 += kv;
-                            y2 = fma(kv, m * Glo[ti], y2);
+                        if (NKRC) { // columns s < 32 have mask 1 in every view: unrolled, no bound
+#pragma unroll
+                            for (int r = 0; r < RB; ++r) {
+                                const int sx = sc0 + 8 * r;
+                                const int ti = X == 0 ? ot * S + sx : sx * S + ot;
+                                const double kv = fma(wq, Td[ti], T5[ti]) * vt[static_cast<size_t>(sx) * QP];
+                                y1 += kv;
+                                y2 = fma(kv, Glo[ti], y2);
+                            }
+                            if (sc0 == 0 && kzs >= ot) { // s == 32: the view's diagonal weight
+                                const int ti = ot * S + ot;
+                                const double m = V == 2 ? 1.0 : (V == 1 ? 0.5 : 0.0);
+                                const double kv = fma(wq, Td[ti], T5[ti]) * vt[static_cast<size_t>(ot) * QP];
+                                y1 += kv;
+                                y2 = fma(kv, m * Glo[ti], y2);
+                            }
+                        } else {
+                            for (int sx = sc0; sx <= kzs; sx += 8) {
+                                const int ti = X == 0 ? ot * S + sx : sx * S + ot;
+                                const double m = V == 2 ? (sx <= ot ? 1.0 : 0.0)
+                                                        : (sx < ot ? 1.0 : (V == 1 && sx == ot ? 0.5 : 0.0));
+                                const double kv = fma(wq, Td[ti], T5[ti]) * vt[static_cast<size_t>(sx) * QP];
+                                y1 += kv;
+                                y2 = fma(kv, m * Glo[ti], y2);
+                            }
                         }
 #pragma unroll
                         for (int d = 1; d < 8; d <<= 1) {
