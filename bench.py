@@ -28,7 +28,9 @@ parity     that sample's reference output against the GPU output of the timed
            configuration at the same points (SURVEY 8(c) bar), counters exact
 exact      FSBM_NUMERICS_EXACT (bitwise coal_step) throughput at C2 + bitwise check
 configs    C3 / C4 (66 / 132 bins, C2 grid) and one GPU's C5 patch (264 bins), each
-           with value, roofline, cpu_baseline and parity (N=1 only)
+           with value, roofline, cpu_baseline and parity (N=1 only); C2-dense (every bin
+           non-zero: no zero-product skips); C2-bott (the C2 workload through Bott's flux
+           method, FSBM_NUMERICS_BOTT, checked against the C port oracle/bott_oracle.c)
 
 --impl reference runs the reference alone (rank 0): oracle/_ref's fissioned_step on a
 bounded sample of the same workload; its inputs come from the checkers under oracle/
@@ -80,7 +82,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip cpu_baseline and parity")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
-    ap.add_argument("--configs", default="C3,C4,C5,C2-dense")
+    ap.add_argument("--configs", default="C3,C4,C5,C2-dense,C2-bott")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cfg-cpu-seconds", type=float, default=5.0)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -177,6 +179,35 @@ class RefCase:
         if st != 0:
             raise RuntimeError(f"reference fissioned_step failed: {self.R.last_error()}")
         return int(cnt[1]) / tim[0], [int(v) for v in cnt], float(tim[0]), cores
+
+
+class BottCase:
+    """CPU port of Bott's flux method (oracle/bott_oracle.c; the reference has no such scheme,
+    SPEC.md:226), same tables as RefCase, all host threads."""
+
+    def __init__(self, nkr):
+        po = checkers()
+        self.O = po.Oracle()
+        self.nkr = nkr
+        self.ratio = po.equal_range_ratio(nkr)
+        self.x = self.O.mass_grid(nkr, X1, self.ratio)
+        self.t750, self.t500 = self.O.build_tables(self.x, npairs=20, family=1, coeff=1.0,
+                                                   level_scale=1.5, pair_scale_step=0.05)
+        self.abd = self.O.default_registry()
+        self.lo = self.O.gain_table(self.x, self.ratio)[0]
+        self.cour = self.O.bott_courant(self.x, self.lo)
+
+    def run(self, ri, nk, njs, T, P, B):
+        cores = os.cpu_count() or 1
+        mask, _ = self.O.fission_predicates(np.ascontiguousarray(T))
+        t0 = time.perf_counter()
+        st, cnt = self.O.bott_step_grid(self.x, self.abd, self.t750, self.t500, self.lo, self.cour,
+                                        mask, np.ascontiguousarray(P), B, CONFIG["dt"],
+                                        CONFIG["substeps"], 1, cores)
+        secs = time.perf_counter() - t0
+        if st != 0:
+            raise RuntimeError("oracle bott_step_grid failed")
+        return int(cnt[1]) / secs, [int(v) for v in cnt], secs, cores
 
 
 def sample_index(ni, nk, nj, ri, njs):
@@ -422,6 +453,41 @@ def sample_parity(fsbm, ctx, grid, ref, dims, T, P, pristine, out_bins, seconds,
     return cpu, par
 
 
+def bott_sample_parity(fsbm, ctx, grid, dims, T, P, pristine, out_bins, seconds, dev):
+    """cpu_baseline (the C port of Bott's scheme on all host threads, kind "port") and parity
+    of the GPU's Bott output against it on one bounded sample of the same bytes."""
+    import torch
+    ni, nk, nj = dims
+    nkr = grid.nkr()
+    bc = BottCase(nkr)
+    cal = size_sample(ni, nk, nj, 2000)
+    idx = sample_index(ni, nk, nj, *cal)
+    B = gather(pristine, torch.from_numpy(idx).to(dev), nkr).cpu().numpy()
+    rate0, _, _, _ = bc.run(cal[0], nk, cal[1], T[idx], P[idx], B)
+    ri, njs = size_sample(ni, nk, nj, int(rate0 * seconds))
+    idx = sample_index(ni, nk, nj, ri, njs)
+    idx_t = torch.from_numpy(idx).to(dev)
+    B_in = gather(pristine, idx_t, nkr).cpu().numpy()
+    ref_out = np.ascontiguousarray(B_in.copy())
+    rate, cnt_ref, secs, cores = bc.run(ri, nk, njs, T[idx], P[idx], ref_out)
+    got = gather(out_bins, idx_t, nkr)
+    sub = fsbm.Ranges(1, ri, 1, nk, 1, njs)
+    cnt = fsbm.WorkCounters()
+    st = fsbm.GridState(sub, grid, torch.from_numpy(T[idx]).to(dev), torch.from_numpy(P[idx]).to(dev),
+                        [torch.from_numpy(B_in[c].reshape(-1)).to(dev) for c in range(6)])
+    fsbm.fissioned_step(st, None, fsbm.StepContext(ctx, counters=cnt),
+                        fsbm.ExecPlan("parallel", 3, 1, "on_demand", "arena", "bott"))
+    del st
+    desc = f"{ri} i-row(s) x {nk} k x {njs} j ({idx.size} points): the grid's first points"
+    par = parity_block(got, ref_out, B_in, grid.x, [cnt.triples, cnt.points, cnt.kernel_evals],
+                       cnt_ref, None, desc)
+    par["checker"] = "oracle/bott_oracle.c (KAT-pinned restatement of Bott 1998; no reference scheme)"
+    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{desc} of this workload, same input bytes; oracle bott_step_grid with {cores} "
+                     f"threads; {secs:.2f} s wall"}
+    return cpu, par
+
+
 def regen(lib, ctx, state, mask, offset, seed, dense, stream):
     """Re-generate a config's input in place (outside the timed events)."""
     import ctypes as C
@@ -473,8 +539,10 @@ def timed_steps(fsbm, lib, ctx, state, mask, plan, steps, prep, stream, dt=CONFI
             cnt)
 
 
-def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_rows=0):
-    """One secondary BASELINE config on this GPU: value, roofline, cpu_baseline, parity."""
+def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_rows=0,
+               numerics="fast"):
+    """One secondary BASELINE config on this GPU: value, roofline, cpu_baseline, parity.
+    numerics="bott": the same workload through Bott's flux method."""
     import torch
 
     import paper_2409_07232_b200 as fsbm
@@ -488,7 +556,7 @@ def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_r
     state, mask = synth.thunderstorm_device(ctx, ni, nk, nj, args.cf, CONFIG["seed"], device=dev,
                                             thermo=(T, P, None))
     stream = torch.cuda.current_stream(dev)
-    plan = fsbm.ExecPlan("parallel", 3, 1, "on_demand", "arena", "fast")
+    plan = fsbm.ExecPlan("parallel", 3, 1, "on_demand", "arena", numerics)
 
     def prep():
         regen(lib, ctx, state, mask, 0, CONFIG["seed"], dense, stream.cuda_stream)
@@ -498,15 +566,27 @@ def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_r
     step_ms, kern_ms, _, cnt = timed_steps(fsbm, lib, ctx, state, mask, plan, steps, prep, stream,
                                            dt)
     points, triples = cnt.points / steps, cnt.triples / steps
+    kname = ctx.fast_kernel() if numerics == "fast" else f"coal_{numerics}"
     out = {"workload": f"{label}: {ni}x{nj}x{nk} (i x j x k), {nkr} bins, "
                        f"{'dense' if dense else 'thunderstorm'} all-category input, cf {args.cf}, "
-                       f"dt {dt:g} s",
+                       f"dt {dt:g} s" + (", Bott (1998) flux method" if numerics == "bott" else ""),
            "value": points / (step_ms * 1e-3), "unit": UNIT, "ms_per_step": step_ms,
            "steps": steps, "updates_per_step": points,
-           "roofline": roofline(nkr, triples, points, kern_ms, peak, ctx.fast_kernel(),
-                                tag=f"{nkr}-dense" if dense else None)}
+           "roofline": roofline(nkr, triples, points, kern_ms, peak, kname,
+                                tag=f"{nkr}-dense" if dense else (f"{nkr}-{numerics}" if numerics != "fast" else None))}
     out["roofline"]["kernel_share_of_step"] = kern_ms / step_ms
-    if not args.no_cpu and not dense:
+    if numerics == "bott":
+        out["roofline"]["note"] = ("SURVEY 8(d)'s 12 FLOP per visited triple, the same work unit as "
+                                   "Kovetz-Olund; Bott's sweep is sequential per point (Gauss-Seidel) "
+                                   "and adds log/exp per non-zero triple: latency-bound, one point per thread")
+    if not args.no_cpu and not dense and numerics == "bott":
+        prep()
+        pristine = [b.clone() for b in state.bins]
+        fsbm.fissioned_step(state, mask, fsbm.StepContext(ctx, stream=stream.cuda_stream), plan)
+        out["cpu_baseline"], out["parity"] = bott_sample_parity(fsbm, ctx, grid, dims, T, P, pristine,
+                                                                state.bins, args.cfg_cpu_seconds, dev)
+        del pristine
+    elif not args.no_cpu and not dense:
         prep()
         pristine = [b.clone() for b in state.bins]
         fsbm.fissioned_step(state, mask, fsbm.StepContext(ctx, stream=stream.cuda_stream), plan)
@@ -680,6 +760,9 @@ def run_ours(args):
                 elif lab == "C2-dense":
                     configs[lab] = run_config(args, "C2 dense input", 33, (425, 50, 300), dev,
                                               peak, dense=True)
+                elif lab == "C2-bott":
+                    configs[lab] = run_config(args, "C2 Bott", 33, (425, 50, 300), dev, peak,
+                                              steps=2, numerics="bott")
             except Exception as ex:
                 configs[lab] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()

@@ -48,10 +48,14 @@ typedef struct {
  * only the kernel_evals counter, kernels.cpp:154-172); scratch_strategy:
  * 0 automatic, 1 arena.  numerics: FSBM_NUMERICS_FAST (FP64, reassociated
  * sums; <=1e-12 relative per bin vs the reference) or FSBM_NUMERICS_EXACT
- * (bitwise identical to coal_step: same operation order, no FMA). */
+ * (bitwise identical to coal_step: same operation order, no FMA).
+ * FSBM_NUMERICS_BOTT replaces the Kovetz-Olund split by Bott's (1998) flux method (the
+ * WRF coal_bott_new scheme the reference declares out of scope): same
+ * inputs, registry order and counters; positive-definite (never FSBM_STIFFNESS);
+ * checked against oracle/bott_oracle.c. */
 enum { FSBM_PRECOMPUTED = 0, FSBM_ON_DEMAND = 1 };
 enum { FSBM_AUTOMATIC = 0, FSBM_ARENA = 1 };
-enum { FSBM_NUMERICS_FAST = 0, FSBM_NUMERICS_EXACT = 1 };
+enum { FSBM_NUMERICS_FAST = 0, FSBM_NUMERICS_EXACT = 1, FSBM_NUMERICS_BOTT = 2 };
 typedef struct {
     int mode;
     int collapse;

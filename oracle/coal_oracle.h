@@ -13,6 +13,7 @@
 #ifndef FSBM_COAL_ORACLE_H
 #define FSBM_COAL_ORACLE_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -85,6 +86,26 @@ int orc_step_grid(int ni, int nk, int nj, int nkr, const double *x, int npairs, 
                   const uint8_t *mask, const double *pressure, double *bins, double dt,
                   int substeps, int kernel_strategy, int nthreads, uint64_t *counters,
                   int *err5);
+
+/* ---- Bott (1998) flux method, multi-category FSBM form (oracle/bott_oracle.c) ----
+ * No reference implementation exists: pinned by known-answer tests. */
+/* Courant numbers [i*nkr+j] of the flux targets g_lo (GainTable lo; 0 for top cells). */
+int orc_bott_courant(int nkr, const double *x, const int32_t *g_lo, double *cour);
+/* Bott's eq. 13 flux of gsk from bin k (after the gain: gk) into bin k+1 (gkp). */
+double orc_bott_flux(double gsk, double gk, double gkp, double c);
+/* One coal step with Bott's flux method instead of Kovetz-Olund; same inputs, counters
+ * and registry semantics as orc_coal_step.  Never raises stiffness (positive-definite). */
+int orc_bott_step(int nkr, const double *x, int npairs, const int *abd, const double *t750,
+                  const double *t500, const int32_t *g_lo, const double *cour,
+                  double *const bins[ORC_NCAT], double pressure, double dt, int substeps,
+                  int kernel_strategy, uint64_t *counters);
+/* orc_bott_step at every mask-true point (mask nullable) of np points; bins category-major
+ * [6][np*nkr]; nthreads contiguous point ranges. */
+int orc_bott_step_grid(size_t np, int nkr, const double *x, int npairs, const int *abd,
+                       const double *t750, const double *t500, const int32_t *g_lo,
+                       const double *cour, const uint8_t *mask, const double *pressure,
+                       double *bins, double dt, int substeps, int kernel_strategy, int nthreads,
+                       uint64_t *counters);
 
 #ifdef __cplusplus
 }

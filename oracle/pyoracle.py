@@ -76,6 +76,15 @@ class Oracle:
                                              C.c_void_p, _dp]
         L.orc_fission_predicates.argtypes = [C.c_uint64, _dp, _u8p]
         L.orc_fission_predicates.restype = C.c_uint64
+        L.orc_bott_courant.argtypes = [C.c_int, _dp, _ip, _dp]
+        L.orc_bott_flux.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double]
+        L.orc_bott_flux.restype = C.c_double
+        L.orc_bott_step.argtypes = [C.c_int, _dp, C.c_int, _ip, _dp, _dp, _ip, _dp,
+                                    C.POINTER(C.c_void_p), C.c_double, C.c_double, C.c_int,
+                                    C.c_int, _u64p]
+        L.orc_bott_step_grid.argtypes = [C.c_size_t, C.c_int, _dp, C.c_int, _ip, _dp, _dp, _ip,
+                                         _dp, C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.c_int,
+                                         C.c_int, _u64p]
         L.orc_step_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _ip, _dp,
                                     _dp, _ip, _dp, _dp, _dp, _u8p, _dp, _dp, C.c_double, C.c_int,
                                     C.c_int, C.c_int, _u64p, _ip]
@@ -138,6 +147,43 @@ class Oracle:
                                     ptrs, pressure, dt, substeps, kernel_strategy, cnt,
                                     C.byref(ec), C.byref(eb))
         return st, cnt, (ec.value, eb.value)
+
+    # ---- Bott (1998) flux method (oracle/bott_oracle.c; parity unpinned: KAT-pinned) ----
+    def bott_courant(self, x, lo):
+        nkr = len(x)
+        cour = np.zeros(nkr * nkr)
+        assert self.lib.orc_bott_courant(nkr, x, np.ascontiguousarray(lo, np.int32), cour) == 0
+        return cour
+
+    def bott_flux(self, gsk, gk, gkp, c):
+        return self.lib.orc_bott_flux(gsk, gk, gkp, c)
+
+    def bott_step(self, x, abd, t750, t500, lo, cour, bins6, pressure, dt=1.0, substeps=1,
+                  kernel_strategy=1):
+        """bins6: (6, nkr) float64, updated in place.  Returns (status, counters)."""
+        nkr = len(x)
+        assert bins6.shape == (NCAT, nkr) and bins6.flags.c_contiguous
+        ptrs = (C.c_void_p * NCAT)(*[bins6[c].ctypes.data for c in range(NCAT)])
+        cnt = np.zeros(3, np.uint64)
+        st = self.lib.orc_bott_step(nkr, x, len(abd) // 3, abd, t750, t500,
+                                    np.ascontiguousarray(lo, np.int32), cour, ptrs, pressure, dt,
+                                    substeps, kernel_strategy, cnt)
+        return st, cnt
+
+    def bott_step_grid(self, x, abd, t750, t500, lo, cour, mask, P, bins, dt=1.0, substeps=1,
+                       kernel_strategy=1, threads=None):
+        """bins: category-major (6, np, nkr) float64, updated in place.  Returns (st, counters)."""
+        nkr = len(x)
+        npt = bins.shape[1]
+        assert bins.shape == (NCAT, npt, nkr) and bins.flags.c_contiguous
+        cnt = np.zeros(3, np.uint64)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        st = self.lib.orc_bott_step_grid(npt, nkr, x, len(abd) // 3, abd, t750, t500,
+                                         np.ascontiguousarray(lo, np.int32), cour,
+                                         None if m is None else m.ctypes.data,
+                                         np.ascontiguousarray(P, np.float64), bins, dt, substeps,
+                                         kernel_strategy, threads or os.cpu_count() or 1, cnt)
+        return st, cnt
 
     def synthetic_case(self, ni, nk, nj, cloud_fraction, seed, nkr=33, x1=3.35e-14, ratio=2.0,
                        number_density=1e6, spectra=True):
@@ -295,6 +341,43 @@ class Reference:
                                       bins6.reshape(-1), pressure, dt, substeps, kernel_strategy,
                                       scratch_strategy, cnt, err)
         return st, cnt, (int(err[0]), int(err[1]))
+
+    # ---- Bott (1998) flux method (oracle/bott_oracle.c; parity unpinned: KAT-pinned) ----
+    def bott_courant(self, x, lo):
+        nkr = len(x)
+        cour = np.zeros(nkr * nkr)
+        assert self.lib.orc_bott_courant(nkr, x, np.ascontiguousarray(lo, np.int32), cour) == 0
+        return cour
+
+    def bott_flux(self, gsk, gk, gkp, c):
+        return self.lib.orc_bott_flux(gsk, gk, gkp, c)
+
+    def bott_step(self, x, abd, t750, t500, lo, cour, bins6, pressure, dt=1.0, substeps=1,
+                  kernel_strategy=1):
+        """bins6: (6, nkr) float64, updated in place.  Returns (status, counters)."""
+        nkr = len(x)
+        assert bins6.shape == (NCAT, nkr) and bins6.flags.c_contiguous
+        ptrs = (C.c_void_p * NCAT)(*[bins6[c].ctypes.data for c in range(NCAT)])
+        cnt = np.zeros(3, np.uint64)
+        st = self.lib.orc_bott_step(nkr, x, len(abd) // 3, abd, t750, t500,
+                                    np.ascontiguousarray(lo, np.int32), cour, ptrs, pressure, dt,
+                                    substeps, kernel_strategy, cnt)
+        return st, cnt
+
+    def bott_step_grid(self, x, abd, t750, t500, lo, cour, mask, P, bins, dt=1.0, substeps=1,
+                       kernel_strategy=1, threads=None):
+        """bins: category-major (6, np, nkr) float64, updated in place.  Returns (st, counters)."""
+        nkr = len(x)
+        npt = bins.shape[1]
+        assert bins.shape == (NCAT, npt, nkr) and bins.flags.c_contiguous
+        cnt = np.zeros(3, np.uint64)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        st = self.lib.orc_bott_step_grid(npt, nkr, x, len(abd) // 3, abd, t750, t500,
+                                         np.ascontiguousarray(lo, np.int32), cour,
+                                         None if m is None else m.ctypes.data,
+                                         np.ascontiguousarray(P, np.float64), bins, dt, substeps,
+                                         kernel_strategy, threads or os.cpu_count() or 1, cnt)
+        return st, cnt
 
     def synthetic_case(self, ni, nk, nj, cloud_fraction, seed, nkr=33, x1=3.35e-14, ratio=2.0,
                        number_density=1e6):

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT_DIR, "libfsbm_coal.so")
 SOURCES = ["fsbm_coal.cu"]
-HEADERS = ["fsbm_common.cuh", "coal_exact.cuh", "coal_fast.cuh", "coal_dmma.cuh", "coal_dmmag.cuh", "state_io.cuh", "fsbm_group.cuh"]
+HEADERS = ["fsbm_common.cuh", "coal_exact.cuh", "coal_fast.cuh", "coal_dmma.cuh", "coal_dmmag.cuh", "coal_bott.cuh", "state_io.cuh", "fsbm_group.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared",

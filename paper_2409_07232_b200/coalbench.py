@@ -211,7 +211,7 @@ AUTOMATIC, ARENA = 0, 1
 FAST, EXACT = 0, 1
 _KSTRAT = {"precomputed": 0, "on_demand": 1}
 _SSTRAT = {"automatic": 0, "arena": 1}
-_NUM = {"fast": 0, "exact": 1}
+_NUM = {"fast": 0, "exact": 1, "bott": 2}
 
 
 @dataclass
@@ -231,7 +231,7 @@ class ExecPlan:
     threads: int = 1
     kernel_strategy: str = "on_demand"
     scratch_strategy: str = "automatic"
-    numerics: str = "fast"  # fast (<=1e-12 rel) | exact (bitwise coal_step)
+    numerics: str = "fast"  # fast (<=1e-12 rel) | exact (bitwise coal_step) | bott (Bott 1998 flux)
 
     def to_c(self) -> fsbm_plan:
         for k, table in (("kernel_strategy", _KSTRAT), ("scratch_strategy", _SSTRAT),

@@ -25,6 +25,7 @@
 #include "coal_fast.cuh"
 #include "coal_dmma.cuh"
 #include "coal_dmmag.cuh"
+#include "coal_bott.cuh"
 #include "fsbm_common.cuh"
 
 using namespace fsbm;
@@ -79,6 +80,8 @@ struct fsbm_ctx {
     double *d_x = nullptr, *d_k500 = nullptr, *d_kd = nullptr;
     int32_t *d_glo = nullptr;
     double *d_gwlo = nullptr, *d_gwhi = nullptr, *d_gtop = nullptr;
+    double *d_bcour = nullptr; // Bott Courant numbers of the GainTable targets [i][j]
+    double *d_rx = nullptr;    // 1 / x (Bott)
     FastTables fast{};
     DmmaTables dmma{};
     DmmagTables dmmag{};
@@ -156,6 +159,8 @@ void free_ctx(fsbm_ctx *c) {
     cudaFree(c->d_gwlo);
     cudaFree(c->d_gwhi);
     cudaFree(c->d_gtop);
+    cudaFree(c->d_bcour);
+    cudaFree(c->d_rx);
     free_fast_tables(c->fast);
     free_dmma_tables(c->dmma);
     free_dmmag_tables(c->dmmag);
@@ -212,7 +217,8 @@ int validate_plan(const fsbm_plan *plan) {
                                  "(per-call automatic arrays forbid the full collapse)");
     if (plan->kernel_strategy != FSBM_PRECOMPUTED && plan->kernel_strategy != FSBM_ON_DEMAND)
         return fail(FSBM_CONFIG, "exec plan: unknown kernel strategy");
-    if (plan->numerics != FSBM_NUMERICS_FAST && plan->numerics != FSBM_NUMERICS_EXACT)
+    if (plan->numerics != FSBM_NUMERICS_FAST && plan->numerics != FSBM_NUMERICS_EXACT &&
+        plan->numerics != FSBM_NUMERICS_BOTT)
         return fail(FSBM_CONFIG, "exec plan: unknown numerics mode");
     return FSBM_OK;
 }
@@ -380,7 +386,15 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     A.pairs = c->pairs;
 
     if (first) FSBM_CUDA_TRY(cudaEventRecord(c->ev0, s));
-    if (plan->numerics == FSBM_NUMERICS_EXACT) {
+    if (plan->numerics == FSBM_NUMERICS_BOTT) {
+        const size_t blocks = std::min<size_t>((np + kBottThreads - 1) / kBottThreads,
+                                               static_cast<size_t>(c->num_sms) * 8);
+        const size_t warps = blocks * (kBottThreads / 32);
+        if (int st = ensure_arena(c, warps * kNCat * c->nkr * 32 * sizeof(double))) return st;
+        coal_bott_kernel<<<static_cast<int>(blocks), kBottThreads, 0, s>>>(
+            A, BottArgs{c->d_bcour, c->d_x, c->d_rx, c->d_arena});
+        FSBM_CUDA_TRY(cudaGetLastError());
+    } else if (plan->numerics == FSBM_NUMERICS_EXACT) {
         const size_t blocks = std::min<size_t>((np + kExactThreads - 1) / kExactThreads,
                                                static_cast<size_t>(c->num_sms) * 8);
         const size_t warps = blocks * (kExactThreads / 32);
@@ -653,6 +667,19 @@ int fsbm_ctx_create(int device, int nkr, const double *x, double ratio, int npai
     if (!st) st = upload(&c->d_gwlo, c->g_wlo.data(), c->g_wlo.size());
     if (!st) st = upload(&c->d_gwhi, c->g_whi.data(), c->g_whi.size());
     if (!st) st = upload(&c->d_gtop, c->g_top.data(), c->g_top.size());
+    if (!st) { // Bott (1998) eq. 11: log-mass position of x_i + x_j in its GainTable target bin
+        std::vector<double> cour(c->g_lo.size(), 0.0);
+        for (int i = 0; i < nkr; ++i)
+            for (int j = 0; j < nkr; ++j) {
+                const size_t e = static_cast<size_t>(i) * nkr + j;
+                const int k = c->g_lo[e];
+                if (k >= 0) cour[e] = std::log((x[i] + x[j]) / x[k]) / std::log(x[k + 1] / x[k]);
+            }
+        st = upload(&c->d_bcour, cour.data(), cour.size());
+        std::vector<double> rx(nkr);
+        for (int k = 0; k < nkr; ++k) rx[k] = 1.0 / x[k];
+        if (!st) st = upload(&c->d_rx, rx.data(), rx.size());
+    }
     if (!st) {
         if (cudaMalloc(&c->d_sink, 8 * sizeof(unsigned long long)) != cudaSuccess ||
             cudaMallocHost(&c->h_sink, 8 * sizeof(unsigned long long)) != cudaSuccess ||
