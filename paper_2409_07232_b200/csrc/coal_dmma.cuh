@@ -1101,7 +1101,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     const uint32_t p = pidx[q];
                     if (p != 0xffffffffu && (pfail[q] & 1) == 0) {
                         report_stiffness(A, p, cf, o0 + lr, vf);
-                        pfail[q] = 2;
+                        atomicOr(&pfail[q], 2); // bit 1: concurrent writers, bit 0 gates
                     }
                 }
             }
@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                     const uint32_t p = pidx[q];
                     if (v < 0.0 && p != 0xffffffffu && (pfail[q] & 1) == 0) {
                         report_stiffness(A, p, c, ot, v);
-                        pfail[q] = 2;
+                        atomicOr(&pfail[q], 2); // bit 1: concurrent writers, bit 0 gates
                     }
                 }
             if (prefetch) {

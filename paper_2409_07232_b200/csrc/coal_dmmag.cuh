@@ -17,13 +17,16 @@
 // c0 = 1 - x_s / width_o -- and give the hi gain X - Y, carried one row (smem).
 //
 // Execution: the per-pass tables (K500, K750-K500) are pre-arranged in DMMA A-fragment
-// order ([pass][block][k][lane]) and streamed per warp from L2 by 512-byte loads; work
-// units (pass, point group, row block) are taken dynamically by the warps of the TMEM
-// lane quadrant that holds the unit's deltas (tcgen05.ld/st), in pass order, with a
-// per-block ticket that fixes the accumulation order (bitwise determinism).  Zero owner
-// rows and zero stream tails (the reference's rate == 0 skip) drop whole units and K-steps.
-// The K-loops are compiled twice (group-uniform vs per-point pressure weights) and the
-// band step twice (far / non-far); 66/132/264 bins are compiled in.
+// order ([pass][block][k][lane]) and streamed per warp from L2 by 512-byte loads, four
+// K-steps in flight ahead of the DMMAs; work units (pass, point group, row block) are taken
+// dynamically by the warps of the TMEM lane quadrant that holds the unit's deltas
+// (tcgen05.ld/st), in pass order, with a per-block ticket that fixes the accumulation order
+// (bitwise determinism).  The band gains are pre-weighted on the host (A(o-t, s) * c_t per
+// pass, one fragment per (t, K-step) entry of the block) and run one target offset at a
+// time, so a single 8x8 accumulator is live: 16 warps x 128 registers at every band width.
+// Zero owner rows and zero stream tails (the reference's rate == 0 skip) drop whole units
+// and K-steps.  The K-loops are compiled twice (group-uniform vs per-point pressure
+// weights); 66/132/264 bins are compiled in.
 #pragma once
 
 #include <algorithm>
@@ -45,10 +48,11 @@ struct DmmagTables {
     double2 *stages = nullptr;   // [item][block][KS][32] A fragments (K500, Kd)
     double *consts = nullptr;    // x[SR+8] | invw[SR+8] (padded, finite)
     int *cls = nullptr;          // [3 views][nblk] leading far K-steps kf
-    uint16_t *bmask = nullptr;   // [3 views][nblk][KS] gather target-offset masks
-    int *goff = nullptr;         // [3][nblk][KS] first gather fragment of the step
-    int *kg = nullptr;           // [3][nblk][2] K-step range holding gather entries
-    double *gcoef = nullptr;     // [entry][32] gather weight fragments
+    double2 *bstages = nullptr;  // [item][view entry][32] band-gain A fragments pre-weighted:
+                                 // (K500, K750-K500)(o-t, s) * c_t(o-t, s)
+    int *gtk = nullptr;          // gather entries t | ks << 8, per (view, block) sorted by (t, ks)
+    int *grange = nullptr;       // [3][nblk][2] entry range of (view, block) in gtk
+    int bofs[2 * kMaxPairs] = {}; // item -> offset of its band fragments minus its view's first entry
     double *carry_g = nullptr;   // [SMs][6][nblk][16] carry rows of lean (global) launches
 };
 
@@ -56,10 +60,9 @@ inline void free_dmmag_tables(DmmagTables &t) {
     cudaFree(t.stages);
     cudaFree(t.consts);
     cudaFree(t.cls);
-    cudaFree(t.bmask);
-    cudaFree(t.goff);
-    cudaFree(t.kg);
-    cudaFree(t.gcoef);
+    cudaFree(t.bstages);
+    cudaFree(t.gtk);
+    cudaFree(t.grange);
     cudaFree(t.carry_g);
     t = DmmagTables{};
 }
@@ -162,6 +165,24 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
             kg[(V * nblk + b) * 2 + 1] = kgh;
         }
     if (gco.empty()) gco.assign(32, 0.0);
+    // the same entries as one list per (view, block), ordered by target offset t then K-step:
+    // the kernel runs them with one accumulator live (the t-th gain of the unit), folding it
+    // into the emission when t changes
+    std::vector<int2> gl;
+    std::vector<int> gr(static_cast<size_t>(3) * nblk * 2, 0);
+    for (int V = 0; V < 3; ++V)
+        for (int b = 0; b < nblk; ++b) {
+            const size_t vb = static_cast<size_t>(V) * nblk + b;
+            gr[2 * vb] = static_cast<int>(gl.size());
+            for (int t = 0; t < TM; ++t)
+                for (int ks = 0; ks < KS; ++ks) {
+                    const unsigned m = bm[vb * KS + ks];
+                    if (m >> t & 1u)
+                        gl.push_back(int2{goff[vb * KS + ks] + __builtin_popcount(m & ((1u << t) - 1u)), t | ks << 8});
+                }
+            gr[2 * vb + 1] = static_cast<int>(gl.size());
+        }
+    if (gl.empty()) gl.push_back(int2{0, 0});
     // ---- per-pass A fragments: [item][block][ks][lane] (K500, K750-K500) ----
     int nitems = 0;
     for (int p = 0; p < npairs; ++p) {
@@ -188,6 +209,41 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                     }
         }
     }
+    // band-gain fragments per item over its view's entry list: entry (t, ks) of block b holds,
+    // per lane (row r, col c), A(8b+r-t, 4ks+c) * c_t of that cell -- the shifted owner row
+    // and its GainTable weight multiplied once here instead of per point batch
+    int vlo[3];
+    for (int V = 0; V < 3; ++V) vlo[V] = gr[2 * (V * nblk)];
+    std::vector<double2> bst;
+    for (int p = 0; p < npairs; ++p) {
+        const bool self = abd[3 * p] == abd[3 * p + 1];
+        const double *k750 = t750 + p * sq, *k500 = t500 + p * sq;
+        for (int X = 0; X < (self ? 1 : 2); ++X) {
+            const int V = X == 1 ? 2 : (self ? 1 : 0), item = D.item_base[p] + X;
+            D.bofs[item] = static_cast<int>(bst.size() / 32) - vlo[V];
+            for (int b = 0; b < nblk; ++b) {
+                const size_t vb = static_cast<size_t>(V) * nblk + b;
+                for (int n = gr[2 * vb]; n < gr[2 * vb + 1]; ++n) {
+                    const int t = gl[n].y & 255, ks = gl[n].y >> 8;
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int o = 8 * b + (lane >> 2) - t, s = 4 * ks + (lane & 3);
+                        const double c = gco[static_cast<size_t>(gl[n].x) * 32 + lane];
+                        double2 v{0.0, 0.0};
+                        if (c != 0.0 && o >= 0 && o < nkr && s < nkr) {
+                            const int i = X == 0 ? o : s, j = X == 0 ? s : o;
+                            const size_t u = self ? static_cast<size_t>(std::min(i, j)) * nkr + std::max(i, j)
+                                                  : static_cast<size_t>(i) * nkr + j;
+                            v = double2{k500[u] * c, (k750[u] - k500[u]) * c};
+                        }
+                        bst.push_back(v);
+                    }
+                }
+            }
+        }
+    }
+    if (bst.empty()) bst.assign(32, double2{0.0, 0.0});
+    std::vector<int> gtk(gl.size());
+    for (size_t n = 0; n < gl.size(); ++n) gtk[n] = gl[n].y;
     std::vector<double> consts(2 * (SR + 8));
     std::copy(xs.begin(), xs.end(), consts.begin());
     std::copy(iw.begin(), iw.end(), consts.begin() + SR + 8);
@@ -197,7 +253,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     };
     if (!up(&D.stages, st) || !up(&D.consts, consts) || !up(&D.cls, kfv) ||
-        !up(&D.bmask, bm) || !up(&D.goff, goff) || !up(&D.kg, kg) || !up(&D.gcoef, gco)) {
+        !up(&D.bstages, bst) || !up(&D.gtk, gtk) || !up(&D.grange, gr)) {
         free_dmmag_tables(D);
         fast_err() = "dmmag tables: device allocation failed";
         return 6;
@@ -230,9 +286,10 @@ struct DmmagArgs {
     int item_base[kMaxPairs];
     const double2 *stages;
     const double *consts;
-    const int *cls, *goff, *kg;
-    const uint16_t *bmask;
-    const double *gcoef;
+    const int *cls;
+    const double2 *bstages;
+    const int *gtk, *grange;
+    int bofs[2 * kMaxPairs];
 };
 
 constexpr int kGSlotCols = 48; // TMEM columns of one (group, block) delta slot: 6 categories x 4 doubles
@@ -260,32 +317,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     uint32_t *pidx = reinterpret_cast<uint32_t *>(ptrip + NP);                // [NP]
     int *pfail = reinterpret_cast<int *>(pidx + NP);                          // [NP]
     int *kfs = pfail + NP;                                                    // [3][NB]
-    int *kgs = kfs + 3 * NB;                                                  // [3][NB][2]
-    int *ps = kgs + 6 * NB;                                                   // [MP] pass: p | X<<8 | nlive<<16
+    int *ps = kfs + 3 * NB;                                                   // [MP] pass: p | X<<8 | nlive<<16
     int *pcum = ps + MP;                                                      // [4][MP+1] units per quadrant
     int *served = pcum + 4 * (MP + 1);                                        // [G][NB] emitted units
     uint16_t *rnk = reinterpret_cast<uint16_t *>(served + G * NB);            // [MP][NB] emission rank
     double *carry;                                                            // [6][G][NB][16]
-    const int *gofs;                                                          // [3][NB][KS]
-    const uint16_t *bms;                                                      // [3][NB][KS]
     {
         unsigned char *tail = reinterpret_cast<unsigned char *>(rnk + MP * NB);
         tail += (16 - reinterpret_cast<uintptr_t>(tail) % 16) % 16;
-        if (lean) {
-            carry = F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP;
-            gofs = F.goff;
-            bms = F.bmask;
-        } else {
-            carry = reinterpret_cast<double *>(tail);
-            int *g2 = reinterpret_cast<int *>(carry + static_cast<size_t>(kNCat) * NB * NP);
-            uint16_t *b2 = reinterpret_cast<uint16_t *>(g2 + 3 * NB * KS);
-            for (int f = threadIdx.x; f < 3 * NB * KS; f += blockDim.x) {
-                g2[f] = F.goff[f];
-                b2[f] = F.bmask[f];
-            }
-            gofs = g2;
-            bms = b2;
-        }
+        carry = lean ? F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP : reinterpret_cast<double *>(tail);
     }
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
@@ -329,7 +369,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 
     for (int f = tid; f < 2 * (SR + 8); f += nthr) xs[f] = F.consts[f];
     for (int f = tid; f < 3 * NB; f += nthr) kfs[f] = F.cls[f];
-    for (int f = tid; f < 6 * NB; f += nthr) kgs[f] = F.kg[f];
     for (int f = tid; f < kNCat * SR * QP; f += nthr) work[f] = 0.0; // rows >= nkr stay zero
     if (tid < 3) cnt_sh[tid] = 0ull;
     if (wid == 0) { // TMEM (whole SM): the delta slots of every (group, block)
@@ -455,7 +494,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 u = __shfl_sync(0xffffffffu, u, 0);
                 while (pi < NPS && u >= pc[pi + 1]) ++pi;
                 if (pi >= NPS) break;
-                const int pw_ = ps[pi], p = pw_ & 255, X = (pw_ >> 8) & 255, nl = pw_ >> 16;
+                const int pw_ = ps[pi], p = pw_ & 255, X = (pw_ >> 8) & 255;
                 const int iu = quad + 4 * (u - pc[pi]); // unit index b*G + g within the pass
                 const int b = iu / G, g = iu % G;
                 const int slot = iu >> 2;
@@ -484,140 +523,138 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     }
                     const bool uni_rt = __all_sync(0xffffffffu, allu);
                     const int vb = V * NB + b;
-                    const int kf = kfs[vb], kgl = kgs[2 * vb], kgh = kgs[2 * vb + 1];
+                    const int kf = kfs[vb];
                     const int kend = min(KS, (kzs >> 2) + 1);
+                    const int kfe = min(kf, kend);
                     const double iwo = iw[o];
                     const double2 *gi = F.stages + static_cast<size_t>(F.item_base[p] + X) * NB * KS * 32;
                     const double2 *ga = gi + static_cast<size_t>(b) * KS * 32 + lane;
+                    const int g0 = __ldg(F.grange + 2 * vb), g1 = __ldg(F.grange + 2 * vb + 1);
                     // L: loss of non-far steps; Xf/Yf: far steps (sum A v, sum A c0 v), owner rows;
-                    // Z[t]: gain of owner rows o-t into rows o (gather form, far cells excluded)
-                    double L[NT][2], Xf[NT][2], Yf[NT][2], Z[TM][NT][2];
+                    // hz: the band gains of owner rows o-t into rows o (gather form, far cells excluded)
+                    double L[NT][2], Xf[NT][2], Yf[NT][2], hz[NT][2];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            L[nt][e] = Xf[nt][e] = Yf[nt][e] = 0.0;
-#pragma unroll
-                            for (int t = 0; t < TM; ++t) Z[t][nt][e] = 0.0;
-                        }
+                        for (int e = 0; e < 2; ++e) L[nt][e] = Xf[nt][e] = Yf[nt][e] = hz[nt][e] = 0.0;
                     // the K-loops, compiled twice: one pressure weight for the whole group
                     // (uni, the common case) or per-point weights (a group straddling a level)
                     auto kloop = [&](auto UC) {
                         constexpr bool uni = decltype(UC)::value;
-                    auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
+                        auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) {
-                            bv[nt] = W(scat, 4 * ks + lc, qg + 8 * nt + lr);
-                            bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
-                        }
-                    };
-                    auto far_step = [&](int ks, double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
-                        const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
-                        const double a2 = a * c0, ad2 = ad * c0;
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) {
-                            dmma(Xf[nt][0], Xf[nt][1], a, bv[nt]);
-                            dmma(Yf[nt][0], Yf[nt][1], a2, bv[nt]);
-                            if (!uni) {
-                                dmma(Xf[nt][0], Xf[nt][1], ad, bw[nt]);
-                                dmma(Yf[nt][0], Yf[nt][1], ad2, bw[nt]);
+                            for (int nt = 0; nt < NT; ++nt) {
+                                bv[nt] = W(scat, 4 * ks + lc, qg + 8 * nt + lr);
+                                bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
                             }
-                        }
-                    };
-                    auto loss_step = [&](double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) {
-                            dmma(L[nt][0], L[nt][1], a, bv[nt]);
-                            if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
-                        }
-                    };
-                    int ks = 0;
-                    // (1) far steps before any gather entry
-#pragma unroll 4
-                    for (; ks < min(kend, min(kf, kgl)); ++ks) {
-                        const double2 kk = __ldg(ga + ks * 32);
-                        double bv[NT], bw[NT];
-                        loadb(ks, bv, bw);
-                        far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
-                    }
-                    // (2) general steps: far or loss, plus the gather entries of the step.  The
-                    // gather operands (weights, shifted A rows) are loaded first so their L2
-                    // latency overlaps the step's own DMMAs; the next A fragment is prefetched.
-                    {
-                        const int k2end = min(kend, max(kf, kgh));
-                        double2 kkn = ks < k2end ? __ldg(ga + ks * 32) : double2{0.0, 0.0};
-                        // one copy of the step for far K-steps, one for the others: no per-step branch
-                        auto step2 = [&](int ks, auto FC) {
-                            constexpr bool FAR = decltype(FC)::value;
-                            const double2 kk = kkn;
-                            if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
-                            const unsigned gmk = lean ? __ldg(bms + vb * KS + ks) : bms[vb * KS + ks];
-                            const int go = lean ? __ldg(gofs + vb * KS + ks) : gofs[vb * KS + ks];
-                            constexpr int TP = TM <= 6 ? TM : 1; // operands held ahead (registers)
-                            double cpre[TP];
-                            double2 kpre[TP];
-                            {
-                                const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
-                                int rk = 0;
-#pragma unroll
-                                for (int t = 0; t < TP; ++t) {
-                                    const bool ont = gmk >> t & 1u;
-                                    cpre[t] = ont ? __ldg(gc + 32 * rk) : 0.0;
-                                    rk += ont ? 1 : 0;
-                                    const int ot = max(o - t, 0); // rows < 0 carry c == 0
-                                    kpre[t] = ont && t > 0 ? __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
-                                                                   (((ot & 7) << 2) | lc))
-                                                           : double2{0.0, 0.0};
-                                }
-                            }
+                        };
+                        // (A) the owner block's K-steps: far [0, kfe) (X/Y identity), loss [kfe, kend).
+                        // A fragments stream from L2 in chunks of DA, ping-ponged between two
+                        // register sets so the next chunk is in flight during this one's DMMAs.
+                        constexpr int DA = 4;
+                        auto step = [&](int ks, double2 kk) {
                             double bv[NT], bw[NT];
                             loadb(ks, bv, bw);
                             const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
-                            if constexpr (FAR) far_step(ks, a, ad, bv, bw);
-                            else loss_step(a, ad, bv, bw);
-                            if (gmk) { // gather entries: owner row o - t, cell (o - t, 4ks + lc)
-                                const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
-                                int rk = 0;
+                            if (ks < kfe) {
+                                const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
+                                const double a2 = a * c0, ad2 = ad * c0;
 #pragma unroll
-                                for (int t = 0; t < TM; ++t) {
-                                    if (gmk >> t & 1u) {
-                                        double c, at = a, adt = ad;
-                                        if (t < TP) {
-                                            c = cpre[t];
-                                            if (t > 0) {
-                                                at = uni ? fma(wu, kpre[t].y, kpre[t].x) : kpre[t].x;
-                                                adt = kpre[t].y;
-                                            }
-                                        } else {
-                                            c = __ldg(gc + 32 * rk);
-                                            const int ot = max(o - t, 0);
-                                            const double2 k2 = __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
-                                                                     (((ot & 7) << 2) | lc));
-                                            at = uni ? fma(wu, k2.y, k2.x) : k2.x;
-                                            adt = k2.y;
-                                        }
-                                        ++rk;
-                                        const double a2 = at * c, ad2 = adt * c;
-#pragma unroll
-                                        for (int nt = 0; nt < NT; ++nt) {
-                                            dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
-                                            if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
-                                        }
+                                for (int nt = 0; nt < NT; ++nt) {
+                                    dmma(Xf[nt][0], Xf[nt][1], a, bv[nt]);
+                                    dmma(Yf[nt][0], Yf[nt][1], a2, bv[nt]);
+                                    if (!uni) {
+                                        dmma(Xf[nt][0], Xf[nt][1], ad, bw[nt]);
+                                        dmma(Yf[nt][0], Yf[nt][1], ad2, bw[nt]);
                                     }
+                                }
+                            } else {
+#pragma unroll
+                                for (int nt = 0; nt < NT; ++nt) {
+                                    dmma(L[nt][0], L[nt][1], a, bv[nt]);
+                                    if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
                                 }
                             }
                         };
-                        for (; ks < min(k2end, kf); ++ks) step2(ks, std::true_type{});
-                        for (; ks < k2end; ++ks) step2(ks, std::false_type{});
-                    }
-                    // (3) loss-only steps above the band
-#pragma unroll 4
-                    for (; ks < kend; ++ks) {
-                        const double2 kk = __ldg(ga + ks * 32);
-                        double bv[NT], bw[NT];
-                        loadb(ks, bv, bw);
-                        loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
-                    }
+                        {
+                            double2 cur[DA];
+#pragma unroll
+                            for (int j = 0; j < DA; ++j) cur[j] = j < kend ? __ldg(ga + j * 32) : double2{0.0, 0.0};
+                            for (int ks = 0; ks < kend; ks += DA) {
+                                double2 nxt[DA];
+#pragma unroll
+                                for (int j = 0; j < DA; ++j)
+                                    nxt[j] = ks + DA + j < kend ? __ldg(ga + (ks + DA + j) * 32) : double2{0.0, 0.0};
+#pragma unroll
+                                for (int j = 0; j < DA; ++j)
+                                    if (ks + j < kend) step(ks + j, cur[j]);
+#pragma unroll
+                                for (int j = 0; j < DA; ++j) cur[j] = nxt[j];
+                            }
+                        }
+                        // (B) band gathers, one target offset t at a time: entry (t, ks) is the
+                        // pre-weighted A row o-t (cell (o-t, 4ks+lc) times its GainTable weight
+                        // towards bin o) against the K-step's B fragment; the t-th sum is scaled
+                        // by the owner value f(o-t) when t changes.  The unit's entries are
+                        // contiguous and streamed like the owner K-steps.
+                        if (g1 > g0) {
+                            const int ng = g1 - g0;
+                            const double2 *gb = F.bstages + (static_cast<size_t>(F.bofs[F.item_base[p] + X]) + g0) * 32 + lane;
+                            const int *gt = F.gtk + g0;
+                            double Zt[NT][2];
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) Zt[nt][0] = Zt[nt][1] = 0.0;
+                            double2 cur[DA];
+                            int tk[DA];
+#pragma unroll
+                            for (int j = 0; j < DA; ++j) {
+                                cur[j] = j < ng ? __ldg(gb + j * 32) : double2{0.0, 0.0};
+                                tk[j] = j < ng ? __ldg(gt + j) : -1;
+                            }
+                            for (int n = 0; n < ng; n += DA) {
+                                double2 nxt[DA];
+                                int tkn[DA];
+#pragma unroll
+                                for (int j = 0; j < DA; ++j) {
+                                    const bool in = n + DA + j < ng;
+                                    nxt[j] = in ? __ldg(gb + (n + DA + j) * 32) : double2{0.0, 0.0};
+                                    tkn[j] = in ? __ldg(gt + n + DA + j) : -1;
+                                }
+#pragma unroll
+                                for (int j = 0; j < DA; ++j) {
+                                    if (n + j >= ng) break;
+                                    const int t = tk[j] & 255, ks = tk[j] >> 8;
+                                    if (ks < kend) {
+                                        double bv[NT], bw[NT];
+                                        loadb(ks, bv, bw);
+                                        const double a2 = uni ? fma(wu, cur[j].y, cur[j].x) : cur[j].x;
+#pragma unroll
+                                        for (int nt = 0; nt < NT; ++nt) {
+                                            dmma(Zt[nt][0], Zt[nt][1], a2, bv[nt]);
+                                            if (!uni) dmma(Zt[nt][0], Zt[nt][1], cur[j].y, bw[nt]);
+                                        }
+                                    }
+                                    const int tn = j + 1 < DA ? tk[j + 1] : tkn[0]; // -1 past the end
+                                    if (tn < 0 || (tn & 255) != t) { // fold the t-th gain
+                                        const int ot = o - t;
+#pragma unroll
+                                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                                            for (int e2 = 0; e2 < 2; ++e2) {
+                                                const int q = qg + 8 * nt + 2 * lc + e2;
+                                                const double ft = on[nt][e2] && ot >= 0 ? W(fcat, ot, q) : 0.0;
+                                                hz[nt][e2] = fma(ft, Zt[nt][e2], hz[nt][e2]);
+                                                Zt[nt][e2] = 0.0;
+                                            }
+                                    }
+                                }
+#pragma unroll
+                                for (int j = 0; j < DA; ++j) {
+                                    cur[j] = nxt[j];
+                                    tk[j] = tkn[j];
+                                }
+                            }
+                        }
                     };
                     if (uni_rt) kloop(std::true_type{});
                     else kloop(std::false_type{});
@@ -632,16 +669,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             lv[2 * nt + e] = f * (L[nt][e] + Xf[nt][e]);
                             const double hi = f * (Xf[nt][e] - Yf[nt][e]);
                             const double up = __shfl_up_sync(0xffffffffu, hi, 4);
-                            double h = f * (Yf[nt][e] + Z[0][nt][e]);
+                            double h = fma(f, Yf[nt][e], hz[nt][e]);
                             if (lr > 0) h += up;
                             hv[2 * nt + e] = h;
                             Xf[nt][e] = hi; // keep for the carry
-#pragma unroll
-                            for (int t = 1; t < TM; ++t) {
-                                const int ot = o - t;
-                                const double ft = on[nt][e] && ot >= 0 ? W(fcat, ot, q) : 0.0;
-                                hv[2 * nt + e] = fma(ft, Z[t][nt][e], hv[2 * nt + e]);
-                            }
                         }
                     // wait for this block's earlier units (deterministic accumulation order)
                     if (lane == 0)
@@ -720,10 +751,12 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 for (int k = wid; k < nkr; k += NW)
                     for (int q = lane; q < NP; q += 32) {
                         const uint32_t p = pidx[q];
-                        if (p == 0xffffffffu || pfail[q] != 0) continue;
+                        // every failing bin is offered (the sink keeps the first in serial
+                        // order): only bit 0 (dead / failed in an earlier substep) gates
+                        if (p == 0xffffffffu || (pfail[q] & 1) != 0) continue;
                         if (W(c, k, q) < 0.0) {
                             report_stiffness(A, p, c, k, W(c, k, q));
-                            pfail[q] = 2;
+                            atomicOr(&pfail[q], 2);
                         }
                     }
             __syncthreads();
@@ -768,9 +801,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean, bool pad) {
     const size_t MP = 2 * static_cast<size_t>(T.npairs);
     size_t b = (static_cast<size_t>(kNCat) * T.SR * (NP + (pad ? 4 : 0)) + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
-               9 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
+               3 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
                MP * T.nblk * 2 + 16;
-    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double) + 3 * T.nblk * T.KS * 6;
+    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double);
     return b;
 }
 
@@ -809,10 +842,10 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     F.stages = T.stages;
     F.consts = T.consts;
     F.cls = T.cls;
-    F.bmask = T.bmask;
-    F.goff = T.goff;
-    F.kg = T.kg;
-    F.gcoef = T.gcoef;
+    F.bstages = T.bstages;
+    F.gtk = T.gtk;
+    F.grange = T.grange;
+    for (int i = 0; i < 2 * kMaxPairs; ++i) F.bofs[i] = T.bofs[i];
     if (NKRC && NKRC != T.nkr) return -1;
     auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD, NKRC>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
@@ -836,21 +869,21 @@ inline bool dmmag_supported(const DmmagTables &T) {
     return T.stages && T.npairs <= kMaxPairs && g.G > 0 && (T.nblk * g.G - 1) / 4 + 1 <= 512 / kGSlotCols;
 }
 
-/// Returns -1 when this geometry cannot run the general DMMA path.  Warps: 16 (128
-/// registers) for target offsets <= 4, else 12 (168 registers); FSBM_DMMAG_WARPS overrides.
+/// Returns -1 when this geometry cannot run the general DMMA path.  16 warps (128
+/// registers: one band-gain accumulator live at a time); FSBM_DMMAG_WARPS overrides (A/B).
 inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cudaStream_t s) {
     if (!T.stages || A.nkr != T.nkr || !dmmag_supported(T)) return -1;
     const DmmagGeom g = dmmag_geom(T);
-    int nw = T.TM <= 4 ? 16 : 12;
+    int nw = 16;
     if (const char *ev = std::getenv("FSBM_DMMAG_WARPS")) nw = std::max(4, std::min(nw, std::atoi(ev)));
     // the BASELINE grids with their extents compiled in (FSBM_DMMAG_GENERIC=1: A/B)
     if (!std::getenv("FSBM_DMMAG_GENERIC")) {
         if (T.nkr == 66 && T.TM == 4 && g.G == 3 && g.pad && !g.lean)
             return launch_dmmag_t<4, 3, 16, true, 66>(T, A, num_sms, s, nw, false);
         if (T.nkr == 132 && T.TM == 6 && g.G == 1 && g.pad && !g.lean)
-            return launch_dmmag_t<6, 1, 12, true, 132>(T, A, num_sms, s, nw, false);
+            return launch_dmmag_t<6, 1, 16, true, 132>(T, A, num_sms, s, nw, false);
         if (T.nkr == 264 && T.TM == 10 && g.G == 1 && !g.pad && g.lean)
-            return launch_dmmag_t<10, 1, 12, false, 264>(T, A, num_sms, s, nw, true);
+            return launch_dmmag_t<10, 1, 16, false, 264>(T, A, num_sms, s, nw, true);
     }
 #define FSBM_DG(TM_, MW_)                                                                          \
     if (g.pad) {                                                                                   \
@@ -868,8 +901,8 @@ inline int launch_dmmag(const DmmagTables &T, const StepArgs &A, int num_sms, cu
     switch (T.TM) {
     case 2: FSBM_DG(2, 16)
     case 4: FSBM_DG(4, 16)
-    case 6: FSBM_DG(6, 12)
-    case 10: FSBM_DG(10, 12)
+    case 6: FSBM_DG(6, 16)
+    case 10: FSBM_DG(10, 16)
     default: return -1;
     }
 #undef FSBM_DG

@@ -412,9 +412,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
                     const size_t ix = IX(s, c, k, q);
                     const double v = work[ix] + (delta[ix] + dhi[ix]);
                     work[ix] = v;
-                    if (v < 0.0 && pfail[qi] == 0) {
+                    // every failing bin is offered (the sink keeps the first in serial
+                    // order); bit 1 marks the failing substep, only bit 0 gates (set at barriers)
+                    if (v < 0.0 && (pfail[qi] & 1) == 0) {
                         report_stiffness(A, p, c, k, v);
-                        pfail[qi] = 2; // first failing substep marks the point
+                        atomicOr(&pfail[qi], 2); // first failing substep marks the point
                     }
                 }
             }

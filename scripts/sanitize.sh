@@ -9,16 +9,16 @@
 OUT=${1:-gpurun_out/sanitizer}
 mkdir -p "$OUT"
 CS=/usr/local/cuda/bin/compute-sanitizer
-CASES="dmma dmmag66 dmmag264 direct exact host group stiff moments"
+CASES=${CASES:-"dmma dmmag66 dmmag264 direct exact host group stiff moments"}
 SC_LIB=build/ab/synccheck.so
 [ -f $SC_LIB ] || bash scripts/build_variant.sh synccheck paper_2409_07232_b200/csrc -DFSBM_SYNCCHECK_MBAR > /dev/null 2>&1
 : > "$OUT/summary.txt"
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   for c in $CASES; do
     f="$OUT/${tool}_${c}.txt"
     extra=""; envs=""
     [ "$tool" = "memcheck" ] && extra="--leak-check no"
-    [ "$tool" = "racecheck" ] && extra="--racecheck-report analysis --print-limit 1000"
+    [ "$tool" = "racecheck" ] && extra="--racecheck-report analysis"
     [ "$tool" = "synccheck" ] && envs="FSBM_LIB_PATH=$SC_LIB"
     env $envs timeout 900 $CS --tool $tool $extra --print-limit 1000 python scripts/sanitize_cases.py $c > "$f" 2>&1
     rc=$?
