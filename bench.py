@@ -11,7 +11,9 @@ level_scale 1.5, pair_scale_step 0.05), dt = 1 s, substeps = 1.
 
 A step = one fissioned_step phase 2 (coal_step at every mask-true point) over the
 rank's i-slab.  Multi-GPU: i-slabs are independent shards (column-local physics,
-no halo); NCCL only all-reduces the end-of-step diagnostics.  The thunderstorm
+no halo), stepped through the library's device group (fsbm_group_step_device, one group
+per rank) whose only collective is its own NCCL all-reduce of the end-of-step counters
+and diagnostics.  The thunderstorm
 state turns stiff after ~4 steps at dt=1, so every step starts from the same
 input: the state is restored device-to-device (outside the per-step CUDA events)
 before each step.  The state (10 GB) is ~80x the L2, so no extra flush is needed.
@@ -655,10 +657,31 @@ def run_ours(args):
     def mass():
         return torch.stack([(b.view(-1, nkr) * xs).sum() for b in state.bins]).sum()
 
+    # N > 1: the step goes through the library's device group (include/fsbm_coal.h,
+    # fsbm_group_*): one group per rank, counters / first failing point / diagnostics
+    # reduced by the library's own NCCL all-reduce; the NCCL id travels
+    # over torch.distributed.  (FSBM_BENCH_ONE_GPU plumbing runs keep the per-rank path.)
+    group = None
+    if world > 1 and os.environ.get("FSBM_BENCH_ONE_GPU") != "1":
+        from paper_2409_07232_b200 import group as fgroup
+        obj = [fgroup.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        group = fgroup.DeviceGroup(grid, tabs, [local], rank, world, obj[0])
+        gctx = group.ctx_handle(0)
+
+    def one_step(counters=cnt, diagnostics=False):
+        if group is None:
+            fsbm.fissioned_step(state, mask, fsbm.StepContext(ctx, sctx.coal, counters,
+                                                              stream=stream.cuda_stream), plan)
+            return None
+        return group.step_device([state], [mask], step_dt, CONFIG["substeps"], plan,
+                                 counters=counters, diagnostics=diagnostics,
+                                 streams=[stream.cuda_stream])
+
     # ---- warm-up ----
     for _ in range(args.warmup):
         restore()
-        fsbm.fissioned_step(state, mask, sctx, plan)
+        one_step()
     torch.cuda.synchronize()
     # ---- timed ----
     e_beg = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -673,10 +696,10 @@ def run_ours(args):
         for s in range(args.steps):
             restore()
             e_beg[s].record(stream)
-            fsbm.fissioned_step(state, mask, sctx, plan)
+            one_step()
             e_end[s].record(stream)
             km, nl = C.c_float(), C.c_int()
-            lib.fsbm_ctx_last_timing(ctx.handle, C.byref(km), C.byref(nl))
+            lib.fsbm_ctx_last_timing(ctx.handle if group is None else gctx, C.byref(km), C.byref(nl))
             kern_ms.append(km.value)
             launches += nl.value
         torch.cuda.synchronize()
@@ -688,12 +711,18 @@ def run_ours(args):
     # diagnostics (the only collective: one NCCL all-reduce of a few scalars); the state
     # keeps this step's output for the parity leg below
     restore()
-    m0 = mass()
-    fsbm.fissioned_step(state, mask, fsbm.StepContext(ctx, sctx.coal, None, stream=stream.cuda_stream), plan)
-    m1 = mass()
-    diag = shard.reduce_diagnostics(
-        shard.StepDiagnostics(cnt.triples // args.steps, cnt.points // args.steps,
-                              cnt.kernel_evals // args.steps, m0.item(), m1.item()), dist, dev)
+    if group is None:
+        m0 = mass()
+        one_step(counters=None)
+        m1 = mass()
+        diag = shard.reduce_diagnostics(
+            shard.StepDiagnostics(cnt.triples // args.steps, cnt.points // args.steps,
+                                  cnt.kernel_evals // args.steps, m0.item(), m1.item()), dist, dev)
+    else:  # counters and masses already summed over every rank by the library (NCCL)
+        gcnt = fsbm.WorkCounters()
+        gd = one_step(counters=gcnt, diagnostics=True)
+        diag = shard.StepDiagnostics(gcnt.triples, gcnt.points, gcnt.kernel_evals,
+                                     float(gd.mass_before.sum()), float(gd.mass_after.sum()))
     tmax = torch.tensor([step_ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)  # device time: max over ranks
@@ -704,7 +733,9 @@ def run_ours(args):
     # ---- roofline (FP64 pipe; algorithmic flops) ----
     peak = fp64_peak(local)
     kname = ctx.fast_kernel() if args.numerics == "fast" else "coal_exact"
-    roof = roofline(nkr, cnt.triples / args.steps, cnt.points / args.steps, kernel_ms, peak,
+    per_rank = world if group is not None else 1  # group counters are summed over ranks
+    roof = roofline(nkr, cnt.triples / args.steps / per_rank, cnt.points / args.steps / per_rank,
+                    kernel_ms, peak,
                     kname, tag=f"{nkr}-dense" if dense else None)
     roof["kernel_share_of_step"] = kernel_ms / step_ms
 
@@ -781,6 +812,8 @@ def run_ours(args):
                                 "mass_rel_drift": abs(m1g - m0g) / m0g, "wall_s_timed": wall},
                 "exact": exact, "configs": configs}
         print(json.dumps(line), flush=True)
+    if group is not None:
+        group.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -41,6 +41,7 @@
 namespace fsbm {
 
 constexpr int kGNT = 2;      // 8-point N-tiles per warp (16 points per group)
+constexpr int kDmmagPadSteps = 8; // zero fragments after each table: unchecked prefetch overrun
 
 struct DmmagTables {
     int nkr = 0, S = 0, KS = 0, nblk = 0, SR = 0, TM = 0, npairs = 0;
@@ -190,7 +191,9 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
         nitems += abd[3 * p] == abd[3 * p + 1] ? 1 : 2;
     }
     const size_t item_elems = static_cast<size_t>(nblk) * KS * 32;
-    std::vector<double2> st(static_cast<size_t>(nitems) * item_elems, double2{0.0, 0.0});
+    // + kDmmagPadSteps fragments of zeros at the end: the kernel's prefetch reads up to 2 x 4
+    // K-steps past a unit's last one without a bounds check (the values are never used)
+    std::vector<double2> st(static_cast<size_t>(nitems) * item_elems + kDmmagPadSteps * 32, double2{0.0, 0.0});
     const size_t sq = static_cast<size_t>(nkr) * nkr;
     for (int p = 0; p < npairs; ++p) {
         const bool self = abd[3 * p] == abd[3 * p + 1];
@@ -241,7 +244,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
             }
         }
     }
-    if (bst.empty()) bst.assign(32, double2{0.0, 0.0});
+    bst.resize(bst.size() + kDmmagPadSteps * 32, double2{0.0, 0.0}); // prefetch overrun
     std::vector<int> gtk(gl.size());
     for (size_t n = 0; n < gl.size(); ++n) gtk[n] = gl[n].y;
     std::vector<double> consts(2 * (SR + 8));
@@ -579,12 +582,12 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         {
                             double2 cur[DA];
 #pragma unroll
-                            for (int j = 0; j < DA; ++j) cur[j] = j < kend ? __ldg(ga + j * 32) : double2{0.0, 0.0};
+                            for (int j = 0; j < DA; ++j) cur[j] = __ldg(ga + j * 32); // past kend: padding, unused
                             for (int ks = 0; ks < kend; ks += DA) {
                                 double2 nxt[DA];
 #pragma unroll
                                 for (int j = 0; j < DA; ++j)
-                                    nxt[j] = ks + DA + j < kend ? __ldg(ga + (ks + DA + j) * 32) : double2{0.0, 0.0};
+                                    nxt[j] = __ldg(ga + (ks + DA + j) * 32);
 #pragma unroll
                                 for (int j = 0; j < DA; ++j)
                                     if (ks + j < kend) step(ks + j, cur[j]);
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             int tk[DA];
 #pragma unroll
                             for (int j = 0; j < DA; ++j) {
-                                cur[j] = j < ng ? __ldg(gb + j * 32) : double2{0.0, 0.0};
+                                cur[j] = __ldg(gb + j * 32);
                                 tk[j] = j < ng ? __ldg(gt + j) : -1;
                             }
                             for (int n = 0; n < ng; n += DA) {
@@ -617,7 +620,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 #pragma unroll
                                 for (int j = 0; j < DA; ++j) {
                                     const bool in = n + DA + j < ng;
-                                    nxt[j] = in ? __ldg(gb + (n + DA + j) * 32) : double2{0.0, 0.0};
+                                    nxt[j] = __ldg(gb + (n + DA + j) * 32);
                                     tkn[j] = in ? __ldg(gt + n + DA + j) : -1;
                                 }
 #pragma unroll
