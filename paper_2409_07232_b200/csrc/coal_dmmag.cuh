@@ -53,6 +53,11 @@ struct DmmagTables {
                                  // (K500, K750-K500)(o-t, s) * c_t(o-t, s)
     int *gtk = nullptr;          // gather entries t | ks << 8, per (view, block) sorted by (t, ks)
     int *grange = nullptr;       // [3][nblk][2] entry range of (view, block) in gtk
+    // narrow bands (TM <= 4): the per-K-step gather form
+    uint16_t *bmask = nullptr;   // [3 views][nblk][KS] gather target-offset masks
+    int *goff = nullptr;         // [3][nblk][KS] first gather weight fragment of the step
+    int *kg = nullptr;           // [3][nblk][2] K-step range holding gather entries
+    double *gcoef = nullptr;     // [entry][32] gather weight fragments
     int bofs[2 * kMaxPairs] = {}; // item -> offset of its band fragments minus its view's first entry
     double *carry_g = nullptr;   // [SMs][6][nblk][16] carry rows of lean (global) launches
 };
@@ -64,6 +69,10 @@ inline void free_dmmag_tables(DmmagTables &t) {
     cudaFree(t.bstages);
     cudaFree(t.gtk);
     cudaFree(t.grange);
+    cudaFree(t.bmask);
+    cudaFree(t.goff);
+    cudaFree(t.kg);
+    cudaFree(t.gcoef);
     cudaFree(t.carry_g);
     t = DmmagTables{};
 }
@@ -256,7 +265,8 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     };
     if (!up(&D.stages, st) || !up(&D.consts, consts) || !up(&D.cls, kfv) ||
-        !up(&D.bstages, bst) || !up(&D.gtk, gtk) || !up(&D.grange, gr)) {
+        !up(&D.bstages, bst) || !up(&D.gtk, gtk) || !up(&D.grange, gr) || !up(&D.bmask, bm) ||
+        !up(&D.goff, goff) || !up(&D.kg, kg) || !up(&D.gcoef, gco)) {
         free_dmmag_tables(D);
         fast_err() = "dmmag tables: device allocation failed";
         return 6;
@@ -292,6 +302,9 @@ struct DmmagArgs {
     const int *cls;
     const double2 *bstages;
     const int *gtk, *grange;
+    const uint16_t *bmask;
+    const int *goff, *kg;
+    const double *gcoef;
     int bofs[2 * kMaxPairs];
 };
 
@@ -325,10 +338,27 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     int *served = pcum + 4 * (MP + 1);                                        // [G][NB] emitted units
     uint16_t *rnk = reinterpret_cast<uint16_t *>(served + G * NB);            // [MP][NB] emission rank
     double *carry;                                                            // [6][G][NB][16]
+    const int *sgoff = F.goff, *skg = F.kg;                                   // narrow bands: [3][NB][KS], [3][NB][2]
+    const uint16_t *sbm = F.bmask;                                            // narrow bands: [3][NB][KS]
     {
         unsigned char *tail = reinterpret_cast<unsigned char *>(rnk + MP * NB);
         tail += (16 - reinterpret_cast<uintptr_t>(tail) % 16) % 16;
         carry = lean ? F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP : reinterpret_cast<double *>(tail);
+        if constexpr (TM <= 4) { // narrow bands: the per-K-step gather tables in shared memory
+            if (!lean) {
+                int *g2 = reinterpret_cast<int *>(carry + static_cast<size_t>(kNCat) * NB * NP);
+                int *k2 = g2 + 3 * NB * KS;
+                uint16_t *b2 = reinterpret_cast<uint16_t *>(k2 + 6 * NB);
+                for (int f = threadIdx.x; f < 3 * NB * KS; f += blockDim.x) {
+                    g2[f] = F.goff[f];
+                    b2[f] = F.bmask[f];
+                }
+                for (int f = threadIdx.x; f < 6 * NB; f += blockDim.x) k2[f] = F.kg[f];
+                sgoff = g2;
+                skg = k2;
+                sbm = b2;
+            }
+        }
     }
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
@@ -551,9 +581,122 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                 bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
                             }
                         };
+                        if constexpr (TM <= 4) {
+                        // Narrow bands (66 bins): short K-loops whose per-step overhead dominates,
+                        // so the gathers ride in the owner loop (ks-outer, one B load per K-step,
+                        // TM sums live) with the gather weights (pair-independent, L1-resident) and
+                        // the shifted A rows (neighbouring fragments of the same pass) loaded per
+                        // entry; measured faster than the pre-weighted streaming form at this width.
+                        double Z[TM][NT][2];
+#pragma unroll
+                        for (int t = 0; t < TM; ++t)
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) Z[t][nt][0] = Z[t][nt][1] = 0.0;
+                        const int kgl = skg[2 * vb], kgh = skg[2 * vb + 1];
+                        auto far_step = [&](int ks, double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
+                            const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
+                            const double a2 = a * c0, ad2 = ad * c0;
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) {
+                                dmma(Xf[nt][0], Xf[nt][1], a, bv[nt]);
+                                dmma(Yf[nt][0], Yf[nt][1], a2, bv[nt]);
+                                if (!uni) {
+                                    dmma(Xf[nt][0], Xf[nt][1], ad, bw[nt]);
+                                    dmma(Yf[nt][0], Yf[nt][1], ad2, bw[nt]);
+                                }
+                            }
+                        };
+                        auto loss_step = [&](double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) {
+                                dmma(L[nt][0], L[nt][1], a, bv[nt]);
+                                if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
+                            }
+                        };
+                        int ks = 0;
+                        // (1) far steps before any gather entry
+#pragma unroll 4
+                        for (; ks < min(kend, min(kf, kgl)); ++ks) {
+                            const double2 kk = __ldg(ga + ks * 32);
+                            double bv[NT], bw[NT];
+                            loadb(ks, bv, bw);
+                            far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                        }
+                        // (2) steps holding gather entries (far or loss + the entries' DMMAs); the
+                        // gather operands are loaded first, the next A fragment one step ahead
+                        {
+                            const int k2end = min(kend, max(kf, kgh));
+                            double2 kkn = ks < k2end ? __ldg(ga + ks * 32) : double2{0.0, 0.0};
+                            auto step2 = [&](int ks, auto FC) {
+                                constexpr bool FAR = decltype(FC)::value;
+                                const double2 kk = kkn;
+                                if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
+                                const unsigned gmk = sbm[vb * KS + ks];
+                                const int go = sgoff[vb * KS + ks];
+                                double cpre[TM];
+                                double2 kpre[TM];
+                                {
+                                    const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
+                                    int rk = 0;
+#pragma unroll
+                                    for (int t = 0; t < TM; ++t) {
+                                        const bool ont = gmk >> t & 1u;
+                                        cpre[t] = ont ? __ldg(gc + 32 * rk) : 0.0;
+                                        rk += ont ? 1 : 0;
+                                        const int ot = max(o - t, 0); // rows < 0 carry c == 0
+                                        kpre[t] = ont && t > 0 ? __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
+                                                                       (((ot & 7) << 2) | lc))
+                                                               : double2{0.0, 0.0};
+                                    }
+                                }
+                                double bv[NT], bw[NT];
+                                loadb(ks, bv, bw);
+                                const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
+                                if constexpr (FAR) far_step(ks, a, ad, bv, bw);
+                                else loss_step(a, ad, bv, bw);
+                                if (gmk) {
+#pragma unroll
+                                    for (int t = 0; t < TM; ++t) {
+                                        if (gmk >> t & 1u) {
+                                            const double at = t > 0 ? (uni ? fma(wu, kpre[t].y, kpre[t].x) : kpre[t].x) : a;
+                                            const double adt = t > 0 ? kpre[t].y : ad;
+                                            const double a2 = at * cpre[t], ad2 = adt * cpre[t];
+#pragma unroll
+                                            for (int nt = 0; nt < NT; ++nt) {
+                                                dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
+                                                if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
+                                            }
+                                        }
+                                    }
+                                }
+                            };
+                            for (; ks < min(k2end, kf); ++ks) step2(ks, std::true_type{});
+                            for (; ks < k2end; ++ks) step2(ks, std::false_type{});
+                        }
+                        // (3) loss-only steps above the band
+#pragma unroll 4
+                        for (; ks < kend; ++ks) {
+                            const double2 kk = __ldg(ga + ks * 32);
+                            double bv[NT], bw[NT];
+                            loadb(ks, bv, bw);
+                            loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                        }
+#pragma unroll
+                        for (int t = 0; t < TM; ++t) { // the band sums, scaled by the owner value f(o-t)
+                            const int ot = o - t;
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                                for (int e2 = 0; e2 < 2; ++e2) {
+                                    const int q = qg + 8 * nt + 2 * lc + e2;
+                                    const double ft = on[nt][e2] && ot >= 0 ? W(fcat, ot, q) : 0.0;
+                                    hz[nt][e2] = fma(ft, Z[t][nt][e2], hz[nt][e2]);
+                                }
+                        }
+                        } else {
                         // (A) the owner block's K-steps: far [0, kfe) (X/Y identity), loss [kfe, kend).
-                        // A fragments stream from L2 in chunks of DA, ping-ponged between two
-                        // register sets so the next chunk is in flight during this one's DMMAs.
+                        // A fragments stream from L2 in chunks of DA; the next chunk is in flight
+                        // during this one's DMMAs (tables padded: no bounds checks on the loads).
                         constexpr int DA = 4;
                         auto step = [&](int ks, double2 kk) {
                             double bv[NT], bw[NT];
@@ -657,6 +800,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                     tk[j] = tkn[j];
                                 }
                             }
+                        }
                         }
                     };
                     if (uni_rt) kloop(std::true_type{});
@@ -806,7 +950,8 @@ inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean, bool pad
     size_t b = (static_cast<size_t>(kNCat) * T.SR * (NP + (pad ? 4 : 0)) + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
                3 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
                MP * T.nblk * 2 + 16;
-    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double);
+    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double) +
+                    (T.TM <= 4 ? 3 * static_cast<size_t>(T.nblk) * T.KS * 6 + 6 * T.nblk * 4 : 0);
     return b;
 }
 
@@ -848,6 +993,10 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     F.bstages = T.bstages;
     F.gtk = T.gtk;
     F.grange = T.grange;
+    F.bmask = T.bmask;
+    F.goff = T.goff;
+    F.kg = T.kg;
+    F.gcoef = T.gcoef;
     for (int i = 0; i < 2 * kMaxPairs; ++i) F.bofs[i] = T.bofs[i];
     if (NKRC && NKRC != T.nkr) return -1;
     auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD, NKRC>;
