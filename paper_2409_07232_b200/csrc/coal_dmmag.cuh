@@ -390,11 +390,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
 
     // point-minor spectra.  PAD: row pitch NP+4 doubles (= 4 mod 16), so the 4 K rows of a
     // B fragment, the 8 owner rows of an emission and the 8 bins of a load each spread over
-    // all banks (2 wavefronts per 256 B, the minimum).  Otherwise (264-bin lean layout)
-    // bit 3 of the point index is swizzled by the bin's parity, which keeps the B fragments
-    // conflict free.
+    // all banks (2 wavefronts per 256 B, the minimum).  Otherwise (264-bin lean layout, one
+    // 16-point row = 128 B) the point index is XOR-swizzled by 4 x (bin mod 4): the 4 K rows
+    // of a B fragment land on disjoint 32-byte bank groups in each half-warp (conflict free).
     auto W = [&](int c, int s, int q) -> double & {
-        return work[(static_cast<size_t>(c) * SR + s) * QP + (PAD ? q : (q ^ ((s & 1) << 3)))];
+        return work[(static_cast<size_t>(c) * SR + s) * QP + (PAD ? q : (q ^ ((s & 3) << 2)))];
     };
     auto CR = [&](int c, int g, int b, int q) -> double & {
         return carry[((static_cast<size_t>(c) * G + g) * NB + b) * 16 + q];
