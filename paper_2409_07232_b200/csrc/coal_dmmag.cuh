@@ -433,7 +433,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 const uint32_t p = pidx[q];
                 const double *src = A.bins[c] + static_cast<size_t>(p) * nkr;
 #pragma unroll 4
-                for (int k = kc; k < nkr; k += 8) W(c, k, q) = p != 0xffffffffu ? __ldg(src + k) : 0.0;
+                // streaming loads/stores (evict-first): the spectra pass through once, the
+                // L2-resident pass tables (tens of MB at 132-264 bins) stay
+                for (int k = kc; k < nkr; k += 8) W(c, k, q) = p != 0xffffffffu ? __ldcs(src + k) : 0.0;
             }
         }
         __syncthreads();
@@ -919,7 +921,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                 if (p == 0xffffffffu) continue;
                 double *dst = A.bins[c] + static_cast<size_t>(p) * nkr;
 #pragma unroll 4
-                for (int k = kc; k < nkr; k += 8) dst[k] = W(c, k, q);
+                for (int k = kc; k < nkr; k += 8) __stcs(dst + k, W(c, k, q));
             }
         }
         for (int q = tid; q < NP; q += nthr) {

@@ -346,3 +346,24 @@ def test_fast_pressure_fields_and_grids(oracle, nkr, ratio, pmode):
     got = np.stack([b.cpu().numpy().reshape(-1, nkr) for b in dst.bins])
     assert_close(got, Bo, f"nkr{nkr} ratio{ratio} {pmode}")
     assert [cnt.triples, cnt.points, cnt.kernel_evals] == [int(v) for v in cnt_o]
+
+
+@pytest.mark.parametrize("kernel,nkr", [("direct", 33), ("dmma", 33), ("dmmag", 33), ("dmmag", 66),
+                                        ("direct", 66), ("dmmag", 132)])
+def test_stiffness_lowest_bin_every_fast_kernel(oracle, monkeypatch, kernel, nkr):
+    """A strongly stiff step (many bins of many categories fail at every point): each FAST
+    kernel must report the reference's first point AND its first (category, bin) -- every
+    failing bin reaches the sink, whichever warp sees it first (coalescence.cpp:313-328;
+    repeated launches, so a scheduling-dependent skip would show)."""
+    monkeypatch.setenv("FSBM_FAST_KERNEL", kernel)
+    ctx, grid, tabs = make_ctx(nkr, coeff=20000.0)
+    st, mask, B = thunder_host(oracle, ctx, 2, 3, 11, 1.0, 23)
+    s, _, err_o, _ = run_oracle_grid(oracle, ctx, tabs, st, mask, B)
+    assert s == 4
+    want = (tuple(int(v) for v in err_o[2:5]), int(err_o[0]), int(err_o[1]))
+    for _ in range(5):
+        d = device_state(st)
+        with pytest.raises(fsbm.StiffnessError) as ei:
+            fsbm.fissioned_step(d, None, fsbm.StepContext(ctx), fsbm.ExecPlan())
+        e = ei.value
+        assert (e.point, e.category, e.bin) == want, kernel
