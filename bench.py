@@ -662,10 +662,13 @@ def run_ours(args):
     # reduced by the library's own NCCL all-reduce; the NCCL id travels
     # over torch.distributed.  (FSBM_BENCH_ONE_GPU plumbing runs keep the per-rank path.)
     group = None
-    if world > 1 and os.environ.get("FSBM_BENCH_ONE_GPU") != "1":
+    # FSBM_BENCH_GROUP=1 takes the group path at N=1 too (a one-rank group, no NCCL): a
+    # plumbing check of the N>1 code on a one-GPU box
+    if (world > 1 and os.environ.get("FSBM_BENCH_ONE_GPU") != "1") or os.environ.get("FSBM_BENCH_GROUP") == "1":
         from paper_2409_07232_b200 import group as fgroup
-        obj = [fgroup.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        obj = [fgroup.nccl_unique_id() if rank == 0 and world > 1 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
         group = fgroup.DeviceGroup(grid, tabs, [local], rank, world, obj[0])
         gctx = group.ctx_handle(0)
 
