@@ -34,15 +34,19 @@ __device__ inline void flush_counters(const StepArgs &A, unsigned long long tr,
     }
 }
 
-__global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, double *arena) {
+/// da[i] is held in a register across the j loop (its updates, and the gains that land on the
+/// same element, are applied in the reference's order).  (Deltas in shared memory -- 4 warps
+/// per SM -- measured 4x slower: the arena's 32 warps per SM hide its L2 latency.)
+__global__ void __launch_bounds__(kExactThreads, 8) coal_exact_kernel(StepArgs A, double *arena) {
     if (A.stale && *A.stale) return; // stale mask: the step must not touch the state
     const int nkr = A.nkr;
     const uint32_t nact = *A.nactive;
     const int lane = threadIdx.x & 31;
     const size_t gwarp = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     constexpr int L = 32; // lane stride inside the arena
-    double *W = arena + gwarp * static_cast<size_t>(2 * kNCat * nkr * L) + lane;
-    double *Dl = W + static_cast<size_t>(kNCat * nkr * L);
+    const size_t span = static_cast<size_t>(kNCat) * nkr * L;
+    double *W = arena + gwarp * 2 * span + lane;
+    double *Dl = W + span;
     const int npairs = A.pairs.npairs;
     const unsigned long long full_evals = static_cast<unsigned long long>(npairs) * nkr * nkr;
 
@@ -68,8 +72,10 @@ __global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, d
             for (int q = 0; q < npairs; ++q) {
                 const int a = A.pairs.a[q], b = A.pairs.b[q], d = A.pairs.d[q];
                 const bool self = a == b;
-                const double *na = W + a * nkr * L;
-                const double *nb = W + b * nkr * L;
+                // the working copies are read-only during the pass loop (only the deltas are
+                // written): restrict lets their loads run ahead of the delta stores
+                const double *__restrict__ na = W + a * nkr * L;
+                const double *__restrict__ nb = W + b * nkr * L;
                 double *da = Dl + a * nkr * L;
                 double *db = Dl + b * nkr * L;
                 double *dd = Dl + d * nkr * L;
@@ -85,6 +91,12 @@ __global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, d
                     const double *gwl = A.g_wlo + static_cast<size_t>(i) * nkr;
                     const double *gwh = A.g_whi + static_cast<size_t>(i) * nkr;
                     const double *gtp = A.g_top + static_cast<size_t>(i) * nkr;
+                    // da[i] in a register for the row: db[j] never aliases it (a != b, or the
+                    // self diagonal, which updates da[i] itself); a gain landing on (a, i) is
+                    // folded into the register in its place in the update sequence
+                    double dai = da[i * L];
+                    const bool dsa = d == a;
+#pragma unroll 4
                     for (int j = j0; j < nkr; ++j) {
                         // interpolate_kernel: K500 + (K750-K500)*w (kernels.hpp:133-135);
                         // kd holds the (K750-K500) difference, bit-identical.
@@ -95,19 +107,25 @@ __global__ void __launch_bounds__(kExactThreads) coal_exact_kernel(StepArgs A, d
                         if (diagonal) rate = __dmul_rn(rate, 0.5);
                         const double dn = __dmul_rn(rate, A.dt_sub);
                         if (diagonal) {
-                            da[i * L] = __dsub_rn(da[i * L], __dmul_rn(2.0, dn));
+                            dai = __dsub_rn(dai, __dmul_rn(2.0, dn));
                         } else {
-                            da[i * L] = __dsub_rn(da[i * L], dn);
+                            dai = __dsub_rn(dai, dn);
                             db[j * L] = __dsub_rn(db[j * L], dn);
                         }
                         const int lo = __ldg(glo + j);
                         if (lo >= 0) {
-                            dd[lo * L] = __dadd_rn(dd[lo * L], __dmul_rn(dn, __ldg(gwl + j)));
-                            dd[(lo + 1) * L] = __dadd_rn(dd[(lo + 1) * L], __dmul_rn(dn, __ldg(gwh + j)));
+                            const double v0 = __dmul_rn(dn, __ldg(gwl + j)), v1 = __dmul_rn(dn, __ldg(gwh + j));
+                            if (dsa && lo == i) dai = __dadd_rn(dai, v0);
+                            else dd[lo * L] = __dadd_rn(dd[lo * L], v0);
+                            if (dsa && lo + 1 == i) dai = __dadd_rn(dai, v1);
+                            else dd[(lo + 1) * L] = __dadd_rn(dd[(lo + 1) * L], v1);
                         } else {
-                            dd[(nkr - 1) * L] = __dadd_rn(dd[(nkr - 1) * L], __dmul_rn(dn, __ldg(gtp + j)));
+                            const double v = __dmul_rn(dn, __ldg(gtp + j));
+                            if (dsa && nkr - 1 == i) dai = __dadd_rn(dai, v);
+                            else dd[(nkr - 1) * L] = __dadd_rn(dd[(nkr - 1) * L], v);
                         }
                     }
+                    da[i * L] = dai;
                     tr += static_cast<unsigned long long>(nkr - j0);
                 }
             }
