@@ -585,8 +585,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     auto fetch_point = [&](uint32_t hbx, uint32_t &p, double &w) {
         const uint32_t idx = hbx * static_cast<uint32_t>(NPH) + htid;
         const bool live = hbx < F.nbatches && idx < nact;
-        p = live ? A.active[idx] : 0xffffffffu;
-        w = live ? pressure_weight(A.pressure[p]) : 0.0;
+        p = live ? A.active[idx] : 0xffffffffu; // holes of the line-aligned list: 0xffffffff
+        w = p != 0xffffffffu ? pressure_weight(A.pressure[p]) : 0.0;
     };
     __shared__ uint32_t nx_p[kDmmaNP];
     __shared__ double nx_w[kDmmaNP];
@@ -625,8 +625,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
         cp_async_wait_all();
         // pressure-weight mode of the warp's 16 points, once per half-batch (see the pair loop)
         {
+            // holes (padding of a line's last group) take any weight
             const double w0 = wts[qg], wl = wts[qg + (lane & 15)];
-            const int wm = __all_sync(0xffffffffu, wl == 0.0) ? 0 : __all_sync(0xffffffffu, wl == w0) ? 1 : 2;
+            const bool hole = pidx[qg + (lane & 15)] == 0xffffffffu;
+            const int wm = __all_sync(0xffffffffu, hole || wl == 0.0)  ? 0
+                           : __all_sync(0xffffffffu, hole || wl == w0) ? 1
+                                                                       : 2;
             if (lane == 0) wmode_s[wid] = static_cast<unsigned char>(wm);
         }
         half_sync(h);

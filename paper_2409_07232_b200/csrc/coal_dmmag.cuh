@@ -417,8 +417,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
          batch += gridDim.x) {
         for (int q = tid; q < NP; q += nthr) {
             const uint32_t idx = batch * static_cast<uint32_t>(NP) + q;
-            const bool live = idx < nact;
-            const uint32_t p = live ? A.active[idx] : 0xffffffffu;
+            // past the end, or a hole of the line-aligned list (0xffffffff): not a point
+            const uint32_t p = idx < nact ? A.active[idx] : 0xffffffffu;
+            const bool live = p != 0xffffffffu;
             pidx[q] = p;
             wts[q] = live ? pressure_weight(A.pressure[p]) : 0.0;
             pfail[q] = live ? 0 : 1;
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         for (int e = 0; e < 2; ++e) {
                             const int q = qg + 8 * nt + 2 * lc + e;
                             on[nt][e] = act[q] >> p & 1ull;
-                            allu = allu && wts[q] == wu;
+                            allu = allu && (wts[q] == wu || pidx[q] == 0xffffffffu); // holes: any weight
                         }
                     }
                     const bool uni_rt = __all_sync(0xffffffffu, allu);

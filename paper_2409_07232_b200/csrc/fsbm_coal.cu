@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -271,6 +272,43 @@ __global__ void flags_kernel(size_t n, int ni, int nk, int nj, int ids, int jds,
     }
 }
 
+/// Line-aligned compaction for the batched FAST kernels (coal_dmma / coal_dmmag), pass 1:
+/// line L = (i, k) of nj points; cnt[L] = its flagged points rounded up to 16.
+__global__ void line_count_kernel(int lines, int nj, const uint8_t *flags, uint32_t *cnt, uint32_t pad) {
+    const int lane = threadIdx.x & 31;
+    for (int L = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; L <= lines; L += (gridDim.x * blockDim.x) >> 5) {
+        uint32_t c = 0;
+        if (L < lines)
+            for (int j = lane; j < nj; j += 32) c += flags[static_cast<size_t>(L) * nj + j];
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+        if (lane == 0) cnt[L] = (c + pad - 1u) / pad * pad; // cnt[lines] = 0: the scan's total
+    }
+}
+
+/// Pass 2: line L's flagged points in j order from off[L] (a multiple of 16), then holes
+/// (0xffffffff) up to the next multiple of 16 -- a 16-point group never spans two lines, so
+/// a pressure field constant along j gives every group one weight and a point's FAST result
+/// does not depend on which lines share its batch (the decomposition).
+__global__ void line_scatter_kernel(int lines, int nj, const uint8_t *flags, const uint32_t *off,
+                                    uint32_t *active, uint32_t *nact, uint32_t pad) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    for (int L = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; L < lines; L += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t base = off[L];
+        uint32_t r = 0;
+        for (int j0 = 0; j0 < nj; j0 += 32) {
+            const int j = j0 + lane;
+            const size_t p = static_cast<size_t>(L) * nj + j;
+            const bool f = j < nj && flags[p] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            if (f) active[base + r + __popc(m & below)] = static_cast<uint32_t>(p);
+            r += __popc(m);
+        }
+        for (uint32_t h = r + lane; h < (r + pad - 1u) / pad * pad; h += 32) active[base + h] = 0xffffffffu;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nact = off[lines];
+}
+
 int grid_for(size_t n, int threads = 256) {
     size_t b = (n + threads - 1) / threads;
     return static_cast<int>(std::min<size_t>(std::max<size_t>(b, 1), 148 * 16));
@@ -324,6 +362,13 @@ int begin_step(fsbm_ctx *c, cudaStream_t s) {
     return FSBM_OK;
 }
 
+/// Whether FSBM_NUMERICS_FAST runs a batched kernel (coal_dmma / coal_dmmag) on this context.
+bool fast_batched(const fsbm_ctx *c) {
+    int k = 0;
+    fsbm_ctx_fast_kernel(c, &k);
+    return k == 2 || k == 3;
+}
+
 /// Enqueue the step of i-rows [i0, i1) (0-based, global) whose arrays start at the
 /// given pointers; no host synchronisation.
 int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
@@ -332,14 +377,26 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
                   int ntiles, cudaStream_t s, bool first, bool last) {
     const int ni = i1 - i0;
     const size_t np = static_cast<size_t>(ni) * g.nk * g.nj;
+    // the batched FAST kernels take line-aligned batches (line_count/line_scatter), the
+    // per-point kernels a dense list (CUB select)
+    const bool lined = plan->numerics == FSBM_NUMERICS_FAST && fast_batched(c) &&
+                       !std::getenv("FSBM_DENSE_COMPACTION");
+    const int lines = ni * g.nk;
+    const size_t cap = lined ? np + 15 * static_cast<size_t>(lines) : np; // list length bound
     size_t cub_bytes = 0;
     thrust::counting_iterator<uint32_t> cnt_it(0);
-    cub::DeviceSelect::Flagged(nullptr, cub_bytes, cnt_it, static_cast<uint8_t *>(nullptr),
-                               static_cast<uint32_t *>(nullptr), static_cast<uint32_t *>(nullptr),
-                               static_cast<int>(np), s);
+    if (lined)
+        cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<uint32_t *>(nullptr),
+                                      static_cast<uint32_t *>(nullptr), lines + 1, s);
+    else
+        cub::DeviceSelect::Flagged(nullptr, cub_bytes, cnt_it, static_cast<uint8_t *>(nullptr),
+                                   static_cast<uint32_t *>(nullptr), static_cast<uint32_t *>(nullptr),
+                                   static_cast<int>(np), s);
     const size_t off_active = (np + 255) / 256 * 256;
-    const size_t off_nact = off_active + (np * 4 + 255) / 256 * 256;
-    const size_t off_cub = off_nact + 256;
+    const size_t off_nact = off_active + (cap * 4 + 255) / 256 * 256;
+    const size_t off_lcnt = off_nact + 256;
+    const size_t off_loff = off_lcnt + (lined ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
+    const size_t off_cub = off_loff + (lined ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
     if (int st = ensure_ws(c, slot, off_cub + cub_bytes)) return st;
     char *ws = static_cast<char *>(c->d_ws[slot]);
     uint8_t *flags = reinterpret_cast<uint8_t *>(ws);
@@ -349,8 +406,21 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     flags_kernel<<<grid_for(np), 256, 0, s>>>(np, ni, g.nk, g.nj, g.r.ids + i0, g.r.jds, mask, T,
                                               tl, ntiles, flags, c->d_sink + 4);
     FSBM_CUDA_TRY(cudaGetLastError());
-    cub::DeviceSelect::Flagged(ws + off_cub, cub_bytes, cnt_it, flags, active, nact,
-                               static_cast<int>(np), s);
+    if (lined) {
+        uint32_t *lcnt = reinterpret_cast<uint32_t *>(ws + off_lcnt);
+        uint32_t *loff = reinterpret_cast<uint32_t *>(ws + off_loff);
+        const int lgrid = static_cast<int>(std::min<size_t>((static_cast<size_t>(lines) + 8) / 8, 148 * 16));
+        constexpr uint32_t pad = 16; // one 16-point group per warp tile
+        line_count_kernel<<<lgrid, 256, 0, s>>>(lines, g.nj, flags, lcnt, pad);
+        FSBM_CUDA_TRY(cudaGetLastError());
+        cub::DeviceScan::ExclusiveSum(ws + off_cub, cub_bytes, lcnt, loff, lines + 1, s);
+        FSBM_CUDA_TRY(cudaGetLastError());
+        line_scatter_kernel<<<lgrid, 256, 0, s>>>(lines, g.nj, flags, loff, active, nact, pad);
+        c->last_launches += 2;
+    } else {
+        cub::DeviceSelect::Flagged(ws + off_cub, cub_bytes, cnt_it, flags, active, nact,
+                                   static_cast<int>(np), s);
+    }
     FSBM_CUDA_TRY(cudaGetLastError());
 
     StepArgs A{};
@@ -367,7 +437,7 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     A.dt_sub = dt / substeps;
     A.substeps = substeps;
     A.kernel_strategy = plan->kernel_strategy;
-    A.nactive_host = static_cast<uint32_t>(np); // upper bound; kernels loop on the device count
+    A.nactive_host = static_cast<uint32_t>(cap); // upper bound; kernels loop on the device count
     A.active = active;
     A.nactive = nact;
     for (int q = 0; q < FSBM_NCAT; ++q) A.bins[q] = bins[q];
