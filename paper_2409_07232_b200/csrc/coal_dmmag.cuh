@@ -575,12 +575,21 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         for (int e = 0; e < 2; ++e) L[nt][e] = Xf[nt][e] = Yf[nt][e] = hz[nt][e] = 0.0;
                     // the K-loops, compiled twice: one pressure weight for the whole group
                     // (uni, the common case) or per-point weights (a group straddling a level)
+                    // unpadded (264-bin) layout: the lane's B-fragment row pointers (row 4ks+lc; the
+                    // swizzle depends on the row mod 4 = lc only), so a K-step's B loads are one
+                    // offset away (+1.8% there; the padded layouts measured faster in index form)
+                    const double *vbp[NT];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const int q = qg + 8 * nt + lr;
+                        vbp[nt] = work + (static_cast<size_t>(scat) * SR + lc) * QP + (q ^ (lc << 2));
+                    }
                     auto kloop = [&](auto UC) {
                         constexpr bool uni = decltype(UC)::value;
                         auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
 #pragma unroll
                             for (int nt = 0; nt < NT; ++nt) {
-                                bv[nt] = W(scat, 4 * ks + lc, qg + 8 * nt + lr);
+                                bv[nt] = PAD ? W(scat, 4 * ks + lc, qg + 8 * nt + lr) : vbp[nt][ks * 4 * QP];
                                 bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
                             }
                         };
