@@ -272,41 +272,68 @@ __global__ void flags_kernel(size_t n, int ni, int nk, int nj, int ids, int jds,
     }
 }
 
-/// Line-aligned compaction for the batched FAST kernels (coal_dmma / coal_dmmag), pass 1:
-/// line L = (i, k) of nj points; cnt[L] = its flagged points rounded up to 16.
-__global__ void line_count_kernel(int lines, int nj, const uint8_t *flags, uint32_t *cnt, uint32_t pad) {
-    const int lane = threadIdx.x & 31;
-    for (int L = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; L <= lines; L += (gridDim.x * blockDim.x) >> 5) {
+/// Level-major compaction for the batched FAST kernels (coal_dmma / coal_dmmag).  The list
+/// visits the (i, k) lines in level-major order (k, then i, then j) and each model level k
+/// starts a new 16-point group: holes (0xffffffff) pad a level's last group.  With pressure
+/// constant on a level (the reference's synthetic profile) every group then has one pressure
+/// weight, so a point's FAST arithmetic never depends on which points share its batch -- the
+/// results are bitwise independent of the decomposition -- at <= 15 holes per level.
+/// Pass 1: cnt[k*ni + i] = flagged points of line (i, k); cnt[lines] = 0 (the scan's total).
+__global__ void level_count_kernel(int ni, int nk, int nj, const uint8_t *flags, uint32_t *cnt) {
+    const int lane = threadIdx.x & 31, lines = ni * nk;
+    for (int Lk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; Lk <= lines; Lk += (gridDim.x * blockDim.x) >> 5) {
         uint32_t c = 0;
-        if (L < lines)
-            for (int j = lane; j < nj; j += 32) c += flags[static_cast<size_t>(L) * nj + j];
+        if (Lk < lines) {
+            const size_t L = static_cast<size_t>(Lk % ni) * nk + Lk / ni; // physical line (i, k)
+            for (int j = lane; j < nj; j += 32) c += flags[L * nj + j];
+        }
         for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-        if (lane == 0) cnt[L] = (c + pad - 1u) / pad * pad; // cnt[lines] = 0: the scan's total
+        if (lane == 0) cnt[Lk] = c;
     }
 }
 
-/// Pass 2: line L's flagged points in j order from off[L] (a multiple of 16), then holes
-/// (0xffffffff) up to the next multiple of 16 -- a 16-point group never spans two lines, so
-/// a pressure field constant along j gives every group one weight and a point's FAST result
-/// does not depend on which lines share its batch (the decomposition).
-__global__ void line_scatter_kernel(int lines, int nj, const uint8_t *flags, const uint32_t *off,
-                                    uint32_t *active, uint32_t *nact, uint32_t pad) {
+/// Holes before level k: sum over levels k' < k of (16-rounded - actual) level counts.
+__device__ inline uint32_t level_pad_before(int k, int ni, const uint32_t *off) {
     const int lane = threadIdx.x & 31;
+    uint32_t h = 0;
+    for (int kk = lane; kk < k; kk += 32) {
+        const uint32_t t = off[(kk + 1) * ni] - off[kk * ni];
+        h += ((t + 15u) & ~15u) - t;
+    }
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    return h;
+}
+
+/// Pass 2 (after an exclusive scan of cnt): line (i, k)'s flagged points in j order; the last
+/// line of each level also writes the level's holes.
+__global__ void level_scatter_kernel(int ni, int nk, int nj, const uint8_t *flags, const uint32_t *off,
+                                     uint32_t *active, uint32_t *nact) {
+    const int lane = threadIdx.x & 31, lines = ni * nk;
     const unsigned below = (1u << lane) - 1u;
-    for (int L = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; L < lines; L += (gridDim.x * blockDim.x) >> 5) {
-        const uint32_t base = off[L];
+    const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int Lk = wg; Lk < lines; Lk += (gridDim.x * blockDim.x) >> 5) {
+        const int k = Lk / ni, i = Lk % ni;
+        const uint32_t hole0 = level_pad_before(k, ni, off);
+        const uint32_t base = off[Lk] + hole0;
+        const size_t L = static_cast<size_t>(i) * nk + k;
         uint32_t r = 0;
         for (int j0 = 0; j0 < nj; j0 += 32) {
             const int j = j0 + lane;
-            const size_t p = static_cast<size_t>(L) * nj + j;
+            const size_t p = L * nj + j;
             const bool f = j < nj && flags[p] != 0;
             const unsigned m = __ballot_sync(0xffffffffu, f);
             if (f) active[base + r + __popc(m & below)] = static_cast<uint32_t>(p);
             r += __popc(m);
         }
-        for (uint32_t h = r + lane; h < (r + pad - 1u) / pad * pad; h += 32) active[base + h] = 0xffffffffu;
+        if (i == ni - 1) { // the level's holes
+            const uint32_t t = off[(k + 1) * ni] - off[k * ni], end = off[(k + 1) * ni] + hole0;
+            for (uint32_t h = lane; h < ((t + 15u) & ~15u) - t; h += 32) active[end + h] = 0xffffffffu;
+        }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *nact = off[lines];
+    if (wg == 0) {
+        const uint32_t h = level_pad_before(nk, ni, off);
+        if (lane == 0) *nact = off[lines] + h;
+    }
 }
 
 int grid_for(size_t n, int threads = 256) {
@@ -377,12 +404,12 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
                   int ntiles, cudaStream_t s, bool first, bool last) {
     const int ni = i1 - i0;
     const size_t np = static_cast<size_t>(ni) * g.nk * g.nj;
-    // the batched FAST kernels take line-aligned batches (line_count/line_scatter), the
-    // per-point kernels a dense list (CUB select)
+    // the batched FAST kernels take a level-major list padded per level (level_count ->
+    // scan -> level_scatter), the per-point kernels a dense list (CUB select)
     const bool lined = plan->numerics == FSBM_NUMERICS_FAST && fast_batched(c) &&
                        !std::getenv("FSBM_DENSE_COMPACTION");
     const int lines = ni * g.nk;
-    const size_t cap = lined ? np + 15 * static_cast<size_t>(lines) : np; // list length bound
+    const size_t cap = lined ? np + 15 * static_cast<size_t>(g.nk) : np; // list length bound
     size_t cub_bytes = 0;
     thrust::counting_iterator<uint32_t> cnt_it(0);
     if (lined)
@@ -410,12 +437,11 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
         uint32_t *lcnt = reinterpret_cast<uint32_t *>(ws + off_lcnt);
         uint32_t *loff = reinterpret_cast<uint32_t *>(ws + off_loff);
         const int lgrid = static_cast<int>(std::min<size_t>((static_cast<size_t>(lines) + 8) / 8, 148 * 16));
-        constexpr uint32_t pad = 16; // one 16-point group per warp tile
-        line_count_kernel<<<lgrid, 256, 0, s>>>(lines, g.nj, flags, lcnt, pad);
+        level_count_kernel<<<lgrid, 256, 0, s>>>(ni, g.nk, g.nj, flags, lcnt);
         FSBM_CUDA_TRY(cudaGetLastError());
         cub::DeviceScan::ExclusiveSum(ws + off_cub, cub_bytes, lcnt, loff, lines + 1, s);
         FSBM_CUDA_TRY(cudaGetLastError());
-        line_scatter_kernel<<<lgrid, 256, 0, s>>>(lines, g.nj, flags, loff, active, nact, pad);
+        level_scatter_kernel<<<lgrid, 256, 0, s>>>(ni, g.nk, g.nj, flags, loff, active, nact);
         c->last_launches += 2;
     } else {
         cub::DeviceSelect::Flagged(ws + off_cub, cub_bytes, cnt_it, flags, active, nact,

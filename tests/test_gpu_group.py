@@ -2,8 +2,8 @@
 i-slab and WRF j-patch shards, against one context and against the oracle.
 
 Results are bitwise independent of the decomposition: EXACT always; FAST
-because the batched kernels group points within one (i, k) line (line-aligned compaction),
-so with pressure constant along j -- the reference's synthetic profile -- every group has
+because the batched kernels group points within one model level (level-major compaction),
+so with pressure constant on a level -- the reference's synthetic profile -- every group has
 one weight and a point's arithmetic never depends on its batch partners.  Counters, the
 first failing point and the diagnostics are whole-domain."""
 import numpy as np
