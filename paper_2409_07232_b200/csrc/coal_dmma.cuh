@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
     auto fetch_point = [&](uint32_t hbx, uint32_t &p, double &w) {
         const uint32_t idx = hbx * static_cast<uint32_t>(NPH) + htid;
         const bool live = hbx < F.nbatches && idx < nact;
-        p = live ? A.active[idx] : 0xffffffffu; // holes of the line-aligned list: 0xffffffff
+        p = live ? A.active[idx] : 0xffffffffu; // holes of the level-major list: 0xffffffff
         w = p != 0xffffffffu ? pressure_weight(A.pressure[p]) : 0.0;
     };
     __shared__ uint32_t nx_p[kDmmaNP];

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
          batch += gridDim.x) {
         for (int q = tid; q < NP; q += nthr) {
             const uint32_t idx = batch * static_cast<uint32_t>(NP) + q;
-            // past the end, or a hole of the line-aligned list (0xffffffff): not a point
+            // past the end, or a hole of the level-major list (0xffffffff): not a point
             const uint32_t p = idx < nact ? A.active[idx] : 0xffffffffu;
             const bool live = p != 0xffffffffu;
             pidx[q] = p;
