@@ -30,7 +30,8 @@ parity     that sample's reference output against the GPU output of the timed
            configuration at the same points (SURVEY 8(c) bar), counters exact
 exact      FSBM_NUMERICS_EXACT (bitwise coal_step) throughput at C2 + bitwise check
 configs    C3 / C4 (66 / 132 bins, C2 grid) and one GPU's C5 patch (264 bins), each
-           with value, roofline, cpu_baseline and parity (N=1 only); C2-dense (every bin
+           with value, roofline, cpu_baseline and parity (N=1 only); C2-cf03 (the
+           SURVEY 8(d) imbalance test: a scattered cloud-fraction-0.3 mask); C2-dense (every bin
            non-zero: no zero-product skips); C2-bott (the C2 workload through Bott's flux
            method, FSBM_NUMERICS_BOTT, checked against the C port oracle/bott_oracle.c)
 
@@ -84,7 +85,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip cpu_baseline and parity")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
-    ap.add_argument("--configs", default="C3,C4,C5,C2-dense,C2-bott")
+    ap.add_argument("--configs", default="C3,C4,C5,C2-cf03,C2-dense,C2-bott")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cfg-cpu-seconds", type=float, default=5.0)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -542,7 +543,7 @@ def timed_steps(fsbm, lib, ctx, state, mask, plan, steps, prep, stream, dt=CONFI
 
 
 def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_rows=0,
-               numerics="fast"):
+               numerics="fast", cf=None):
     """One secondary BASELINE config on this GPU: value, roofline, cpu_baseline, parity.
     numerics="bott": the same workload through Bott's flux method."""
     import torch
@@ -553,9 +554,10 @@ def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_r
     ni, nk, nj = dims
     ctx, grid, tabs = make_ctx(nkr, dev.index or 0)
     ni_g = ni if not offset_rows else offset_rows
-    T, P, _ = synth.thermo_host(ni_g, nk, nj, args.cf, CONFIG["seed"], grid)
+    cf = args.cf if cf is None else cf
+    T, P, _ = synth.thermo_host(ni_g, nk, nj, cf, CONFIG["seed"], grid)
     T, P = T[:ni * nk * nj].copy(), P[:ni * nk * nj].copy()
-    state, mask = synth.thunderstorm_device(ctx, ni, nk, nj, args.cf, CONFIG["seed"], device=dev,
+    state, mask = synth.thunderstorm_device(ctx, ni, nk, nj, cf, CONFIG["seed"], device=dev,
                                             thermo=(T, P, None))
     stream = torch.cuda.current_stream(dev)
     plan = fsbm.ExecPlan("parallel", 3, 1, "on_demand", "arena", numerics)
@@ -570,7 +572,7 @@ def run_config(args, label, nkr, dims, dev, peak, steps=3, dense=False, offset_r
     points, triples = cnt.points / steps, cnt.triples / steps
     kname = ctx.fast_kernel() if numerics == "fast" else f"coal_{numerics}"
     out = {"workload": f"{label}: {ni}x{nj}x{nk} (i x j x k), {nkr} bins, "
-                       f"{'dense' if dense else 'thunderstorm'} all-category input, cf {args.cf}, "
+                       f"{'dense' if dense else 'thunderstorm'} all-category input, cf {cf}, "
                        f"dt {dt:g} s" + (", Bott (1998) flux method" if numerics == "bott" else ""),
            "value": points / (step_ms * 1e-3), "unit": UNIT, "ms_per_step": step_ms,
            "steps": steps, "updates_per_step": points,
@@ -791,6 +793,9 @@ def run_ours(args):
                 elif lab == "C5":
                     configs[lab] = run_config(args, "C5 per-GPU patch (106 of 850 i-rows)", 264,
                                               (106, 50, 600), dev, peak, steps=2, offset_rows=850)
+                elif lab == "C2-cf03":  # SURVEY 8(d)'s imbalance test: scattered cf 0.3 mask
+                    configs[lab] = run_config(args, "C2 cloud fraction 0.3", 33, (425, 50, 300), dev,
+                                              peak, cf=0.3)
                 elif lab == "C2-dense":
                     configs[lab] = run_config(args, "C2 dense input", 33, (425, 50, 300), dev,
                                               peak, dense=True)
