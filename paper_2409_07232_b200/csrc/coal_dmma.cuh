@@ -795,11 +795,20 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) coal_dmma_kernel(StepArgs A, 
                         // one instantiation per block (K500 + w*Kd with w = 0 for p <= 500 hPa):
                         // halving the unrolled code keeps the kernel inside the instruction cache
                         const double wi = wmode == 1 ? wu : 0.0;
-                        switch (b) {
-                        case 0: FSBM_PASS(0, true); break;
-                        case 1: FSBM_PASS(1, true); break;
-                        case 2: FSBM_PASS(2, true); break;
-                        default: FSBM_PASS(3, true); break;
+                        if (wmode == 0) { // p <= 500 hPa: A = K500 exactly, no interpolation
+                            switch (b) {
+                            case 0: FSBM_PASS(0, false); break;
+                            case 1: FSBM_PASS(1, false); break;
+                            case 2: FSBM_PASS(2, false); break;
+                            default: FSBM_PASS(3, false); break;
+                            }
+                        } else {
+                            switch (b) {
+                            case 0: FSBM_PASS(0, true); break;
+                            case 1: FSBM_PASS(1, true); break;
+                            case 2: FSBM_PASS(2, true); break;
+                            default: FSBM_PASS(3, true); break;
+                            }
                         }
 #undef FSBM_PASS
                         }
