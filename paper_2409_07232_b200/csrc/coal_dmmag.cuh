@@ -585,7 +585,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         vbp[nt] = work + (static_cast<size_t>(scat) * SR + lc) * QP + (q ^ (lc << 2));
                     }
                     auto kloop = [&](auto UC) {
-                        constexpr bool uni = decltype(UC)::value;
+                        // 0: per-point weights (dual), 1: one weight for the group, 2: that weight is 0
+                        // (p <= 500 hPa: A = K500 exactly, no interpolation)
+                        constexpr int MODE = decltype(UC)::value;
+                        constexpr bool uni = MODE != 0, w0 = MODE == 2;
                         auto loadb = [&](int ks, double (&bv)[NT], double (&bw)[NT]) {
 #pragma unroll
                             for (int nt = 0; nt < NT; ++nt) {
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             const double2 kk = __ldg(ga + ks * 32);
                             double bv[NT], bw[NT];
                             loadb(ks, bv, bw);
-                            far_step(ks, uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                            far_step(ks, uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, kk.y, bv, bw);
                         }
                         // (2) steps holding gather entries (far or loss + the entries' DMMAs); the
                         // gather operands are loaded first, the next A fragment one step ahead
@@ -663,14 +666,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                 }
                                 double bv[NT], bw[NT];
                                 loadb(ks, bv, bw);
-                                const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
+                                const double a = uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, ad = kk.y;
                                 if constexpr (FAR) far_step(ks, a, ad, bv, bw);
                                 else loss_step(a, ad, bv, bw);
                                 if (gmk) {
 #pragma unroll
                                     for (int t = 0; t < TM; ++t) {
                                         if (gmk >> t & 1u) {
-                                            const double at = t > 0 ? (uni ? fma(wu, kpre[t].y, kpre[t].x) : kpre[t].x) : a;
+                                            const double at = t > 0 ? (uni ? (w0 ? kpre[t].x : fma(wu, kpre[t].y, kpre[t].x)) : kpre[t].x) : a;
                                             const double adt = t > 0 ? kpre[t].y : ad;
                                             const double a2 = at * cpre[t], ad2 = adt * cpre[t];
 #pragma unroll
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             const double2 kk = __ldg(ga + ks * 32);
                             double bv[NT], bw[NT];
                             loadb(ks, bv, bw);
-                            loss_step(uni ? fma(wu, kk.y, kk.x) : kk.x, kk.y, bv, bw);
+                            loss_step(uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, kk.y, bv, bw);
                         }
 #pragma unroll
                         for (int t = 0; t < TM; ++t) { // the band sums, scaled by the owner value f(o-t)
@@ -713,7 +716,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         auto step = [&](int ks, double2 kk) {
                             double bv[NT], bw[NT];
                             loadb(ks, bv, bw);
-                            const double a = uni ? fma(wu, kk.y, kk.x) : kk.x, ad = kk.y;
+                            const double a = uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, ad = kk.y;
                             if (ks < kfe) {
                                 const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
                                 const double a2 = a * c0, ad2 = ad * c0;
@@ -785,7 +788,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                     if (ks < kend) {
                                         double bv[NT], bw[NT];
                                         loadb(ks, bv, bw);
-                                        const double a2 = uni ? fma(wu, cur[j].y, cur[j].x) : cur[j].x;
+                                        const double a2 = uni ? (w0 ? cur[j].x : fma(wu, cur[j].y, cur[j].x)) : cur[j].x;
 #pragma unroll
                                         for (int nt = 0; nt < NT; ++nt) {
                                             dmma(Zt[nt][0], Zt[nt][1], a2, bv[nt]);
@@ -815,8 +818,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         }
                         }
                     };
-                    if (uni_rt) kloop(std::true_type{});
-                    else kloop(std::false_type{});
+                    if (!uni_rt) kloop(std::integral_constant<int, 0>{});
+                    else if (wu == 0.0) kloop(std::integral_constant<int, 2>{});
+                    else kloop(std::integral_constant<int, 1>{});
                     // owner emission values (dt at the apply); far-cell hi gains of row 7
                     // carry into the next block's head row
 #pragma unroll
