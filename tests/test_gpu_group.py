@@ -129,3 +129,25 @@ def test_group_stale_mask_and_config_errors(oracle):
                                                                  "automatic"))
     with pytest.raises(fsbm.DomainError):  # more shards than j columns
         fsbm.DeviceGroup(grid, tabs, [0] * 5).step_host(host_copy(st), None, "j")
+
+
+@pytest.mark.parametrize("cf", [0.05, 0.3])
+@pytest.mark.parametrize("nkr", [33, 66])
+def test_group_sparse_masks_bitwise(oracle, cf, nkr):
+    """Sparse scattered masks (most 16-point groups of the level-major list carry holes, many
+    levels hold fewer than 16 active points): counters exact, FAST within the bar, and the
+    j-patch group bitwise equal to one context."""
+    ctx, grid, tabs = make_ctx(nkr)
+    st, mask, B = thunder_host(oracle, ctx, 7, 6, 11, cf, 3)
+    s, cnt_o, _, Bo = run_oracle_grid(oracle, ctx, tabs, st, mask, B)
+    assert s == 0
+    one = host_copy(st)
+    c1 = fsbm.WorkCounters()
+    fsbm.fissioned_step(one, None, fsbm.StepContext(ctx, counters=c1), fsbm.ExecPlan())
+    got1 = np.stack([b.reshape(-1, nkr) for b in one.bins])
+    assert [c1.triples, c1.points, c1.kernel_evals] == [int(v) for v in cnt_o]
+    assert_close(got1, Bo, f"sparse cf {cf}")
+    g = group_for(grid, tabs, (0, 0, 0))
+    two = host_copy(st)
+    g.step_host(two, None, "j")
+    assert np.array_equal(np.stack([b.reshape(-1, nkr) for b in two.bins]), got1)
