@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     coal_fast_kernel(StepArgs A, FastArgs F) {
     using G = FastGeom<R>;
     constexpr int PTS = G::PTS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nkr = A.nkr;
     const int nsets = F.nsets;
     const size_t arr = static_cast<size_t>(nsets) * kNCat * nkr * PTS; // doubles per buffer
