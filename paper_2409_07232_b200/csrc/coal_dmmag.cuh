@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
     __shared__ int kzc[kNCat];
+    __shared__ unsigned char guni[G]; // the group's live points share one pressure weight
     __shared__ int qcnt[4];
     __shared__ int npass;
     __shared__ uint32_t tmem_base;
@@ -437,6 +438,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
             ptrip[q] = 0;
         }
         __syncthreads();
+        if (PAD && wid < G) { // one pressure weight per group (holes: any weight), once per batch
+            const int q = 16 * wid + (lane & 15);
+            const bool u = __all_sync(0xffffffffu, pidx[q] == 0xffffffffu || wts[q] == wts[16 * wid]);
+            if (lane == 0) guni[wid] = u ? 1 : 0;
+        }
         { // spectra -> work: a warp instruction covers 4 points x 8 consecutive bins
             const int NQ = kNCat * NP / 4;
             const int qs = lane >> 3, kc = lane & 7;
@@ -565,10 +571,12 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                         for (int e = 0; e < 2; ++e) {
                             const int q = qg + 8 * nt + 2 * lc + e;
                             on[nt][e] = act[q] >> p & 1ull;
-                            allu = allu && (wts[q] == wu || pidx[q] == 0xffffffffu); // holes: any weight
+                            if (!PAD) allu = allu && (wts[q] == wu || pidx[q] == 0xffffffffu); // holes: any weight
                         }
                     }
-                    const bool uni_rt = __all_sync(0xffffffffu, allu);
+                    // the group's weight mode, found once per batch (padded layouts; the
+                    // register-tight 264-bin layout measured faster re-deriving it per unit)
+                    const bool uni_rt = PAD ? guni[g] != 0 : __all_sync(0xffffffffu, allu);
                     const int vb = V * NB + b;
                     const int kf = kfs[vb];
                     const int kend = min(KS, (kzs >> 2) + 1);
