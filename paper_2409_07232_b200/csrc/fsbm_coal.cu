@@ -406,13 +406,13 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     const size_t np = static_cast<size_t>(ni) * g.nk * g.nj;
     // the batched FAST kernels take a level-major list padded per level (level_count ->
     // scan -> level_scatter), the per-point kernels a dense list (CUB select)
-    const bool lined = plan->numerics == FSBM_NUMERICS_FAST && fast_batched(c) &&
+    const bool level_list = plan->numerics == FSBM_NUMERICS_FAST && fast_batched(c) &&
                        !std::getenv("FSBM_DENSE_COMPACTION");
     const int lines = ni * g.nk;
-    const size_t cap = lined ? np + 15 * static_cast<size_t>(g.nk) : np; // list length bound
+    const size_t cap = level_list ? np + 15 * static_cast<size_t>(g.nk) : np; // list length bound
     size_t cub_bytes = 0;
     thrust::counting_iterator<uint32_t> cnt_it(0);
-    if (lined)
+    if (level_list)
         cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<uint32_t *>(nullptr),
                                       static_cast<uint32_t *>(nullptr), lines + 1, s);
     else
@@ -422,8 +422,8 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     const size_t off_active = (np + 255) / 256 * 256;
     const size_t off_nact = off_active + (cap * 4 + 255) / 256 * 256;
     const size_t off_lcnt = off_nact + 256;
-    const size_t off_loff = off_lcnt + (lined ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
-    const size_t off_cub = off_loff + (lined ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
+    const size_t off_loff = off_lcnt + (level_list ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
+    const size_t off_cub = off_loff + (level_list ? (static_cast<size_t>(lines + 1) * 4 + 255) / 256 * 256 : 0);
     if (int st = ensure_ws(c, slot, off_cub + cub_bytes)) return st;
     char *ws = static_cast<char *>(c->d_ws[slot]);
     uint8_t *flags = reinterpret_cast<uint8_t *>(ws);
@@ -433,7 +433,7 @@ int enqueue_chunk(fsbm_ctx *c, int slot, const StepGeom &g, int i0, int i1,
     flags_kernel<<<grid_for(np), 256, 0, s>>>(np, ni, g.nk, g.nj, g.r.ids + i0, g.r.jds, mask, T,
                                               tl, ntiles, flags, c->d_sink + 4);
     FSBM_CUDA_TRY(cudaGetLastError());
-    if (lined) {
+    if (level_list) {
         uint32_t *lcnt = reinterpret_cast<uint32_t *>(ws + off_lcnt);
         uint32_t *loff = reinterpret_cast<uint32_t *>(ws + off_loff);
         const int lgrid = static_cast<int>(std::min<size_t>((static_cast<size_t>(lines) + 8) / 8, 148 * 16));
