@@ -880,8 +880,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                             Xf[nt][e] = hi; // keep for the carry
                         }
                     // wait for this block's earlier units (deterministic accumulation order)
-                    if (lane == 0)
+                    if (lane == 0) // (a short sleep per poll leaves issue slots to the working warps)
                         while (*reinterpret_cast<volatile int *>(&served[g * NB + b]) != rank) {
+                            __nanosleep(20);
                         }
                     __syncwarp();
                     __threadfence_block();
