@@ -918,6 +918,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     tm_fence_before();
                 } else if (lane == 0) {
                     while (*reinterpret_cast<volatile int *>(&served[g * NB + b]) != rank) {
+                        __nanosleep(20);
                     }
                 }
                 __syncwarp();
