@@ -55,11 +55,6 @@ struct DmmagTables {
                                  // (K500, K750-K500)(o-t, s) * c_t(o-t, s)
     int *gtk = nullptr;          // gather entries t | ks << 8, per (view, block) sorted by (t, ks)
     int *grange = nullptr;       // [3][nblk][2] entry range of (view, block) in gtk
-    // narrow bands (TM <= 4): the per-K-step gather form
-    uint16_t *bmask = nullptr;   // [3 views][nblk][KS] gather target-offset masks
-    int *goff = nullptr;         // [3][nblk][KS] first gather weight fragment of the step
-    int *kg = nullptr;           // [3][nblk][2] K-step range holding gather entries
-    double *gcoef = nullptr;     // [entry][32] gather weight fragments
     int bofs[2 * kMaxPairs] = {}; // item -> offset of its band fragments minus its view's first entry
     double *carry_g = nullptr;   // [SMs][6][nblk][16] carry rows of lean (global) launches
 };
@@ -73,10 +68,6 @@ inline void free_dmmag_tables(DmmagTables &t) {
     cudaFree(t.bstages);
     cudaFree(t.gtk);
     cudaFree(t.grange);
-    cudaFree(t.bmask);
-    cudaFree(t.goff);
-    cudaFree(t.kg);
-    cudaFree(t.gcoef);
     cudaFree(t.carry_g);
     t = DmmagTables{};
 }
@@ -137,14 +128,14 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
             }
             kfv[V * nblk + b] = kf;
         }
-    // gather coefficient fragments (pair-independent): entry (V, b, ks, t) holds, per lane
-    // (row r = lane/4, col c = lane%4), the GainTable weight of cell (8b+r-t, 4ks+c)
-    // towards bin 8b+r, view-masked, zero for far cells (handled by the X/Y identity)
-    std::vector<int> goff(static_cast<size_t>(3) * nblk * KS, 0), kg(3 * nblk * 2, 0);
+    // gather coefficient fragments (pair-independent, host only: they weight the band tables
+    // below): entry (V, b, ks, t) holds, per lane (row r = lane/4, col c = lane%4), the
+    // GainTable weight of cell (8b+r-t, 4ks+c) towards bin 8b+r, view-masked, zero for far
+    // cells (handled by the X/Y identity)
+    std::vector<int> goff(static_cast<size_t>(3) * nblk * KS, 0);
     std::vector<double> gco;
     for (int V = 0; V < 3; ++V)
         for (int b = 0; b < nblk; ++b) {
-            int kgl = KS, kgh = 0;
             for (int ks = 0; ks < KS; ++ks) {
                 double frag[16][32] = {};
                 uint16_t mask = 0;
@@ -170,13 +161,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
                 goff[(static_cast<size_t>(V) * nblk + b) * KS + ks] = static_cast<int>(gco.size() / 32);
                 for (int t = 0; t < TM; ++t)
                     if (mask >> t & 1u) gco.insert(gco.end(), frag[t], frag[t] + 32);
-                if (mask) {
-                    kgl = std::min(kgl, ks);
-                    kgh = ks + 1;
-                }
             }
-            kg[(V * nblk + b) * 2] = std::min(kgl, kgh);
-            kg[(V * nblk + b) * 2 + 1] = kgh;
         }
     if (gco.empty()) gco.assign(32, 0.0);
     // the same entries as one list per (view, block), ordered by target offset t then K-step:
@@ -276,8 +261,7 @@ inline int build_dmmag_tables(DmmagTables &D, int nkr, int npairs, const std::ve
     for (auto &v : bst1) v.x = v.x + v.y;
     if (!up(&D.stages, st) || !up(&D.consts, consts) || !up(&D.cls, kfv) || !up(&D.stages1, st1) ||
         !up(&D.bstages1, bst1) ||
-        !up(&D.bstages, bst) || !up(&D.gtk, gtk) || !up(&D.grange, gr) || !up(&D.bmask, bm) ||
-        !up(&D.goff, goff) || !up(&D.kg, kg) || !up(&D.gcoef, gco)) {
+        !up(&D.bstages, bst) || !up(&D.gtk, gtk) || !up(&D.grange, gr)) {
         free_dmmag_tables(D);
         fast_err() = "dmmag tables: device allocation failed";
         return 6;
@@ -313,9 +297,6 @@ struct DmmagArgs {
     const int *cls;
     const double2 *bstages, *bstages1;
     const int *gtk, *grange;
-    const uint16_t *bmask;
-    const int *goff, *kg;
-    const double *gcoef;
     int bofs[2 * kMaxPairs];
 };
 
@@ -349,27 +330,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
     int *served = pcum + 4 * (MP + 1);                                        // [G][NB] emitted units
     uint16_t *rnk = reinterpret_cast<uint16_t *>(served + G * NB);            // [MP][NB] emission rank
     double *carry;                                                            // [6][G][NB][16]
-    const int *sgoff = F.goff, *skg = F.kg;                                   // narrow bands: [3][NB][KS], [3][NB][2]
-    const uint16_t *sbm = F.bmask;                                            // narrow bands: [3][NB][KS]
     {
         unsigned char *tail = reinterpret_cast<unsigned char *>(rnk + MP * NB);
         tail += (16 - reinterpret_cast<uintptr_t>(tail) % 16) % 16;
         carry = lean ? F.carry_g + static_cast<size_t>(blockIdx.x) * kNCat * NB * NP : reinterpret_cast<double *>(tail);
-        if constexpr (TM <= 4) { // narrow bands: the per-K-step gather tables in shared memory
-            if (!lean) {
-                int *g2 = reinterpret_cast<int *>(carry + static_cast<size_t>(kNCat) * NB * NP);
-                int *k2 = g2 + 3 * NB * KS;
-                uint16_t *b2 = reinterpret_cast<uint16_t *>(k2 + 6 * NB);
-                for (int f = threadIdx.x; f < 3 * NB * KS; f += blockDim.x) {
-                    g2[f] = F.goff[f];
-                    b2[f] = F.bmask[f];
-                }
-                for (int f = threadIdx.x; f < 6 * NB; f += blockDim.x) k2[f] = F.kg[f];
-                sgoff = g2;
-                skg = k2;
-                sbm = b2;
-            }
-        }
     }
     __shared__ unsigned long long cta_act;
     __shared__ int kzg[G][kNCat];
@@ -583,7 +547,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                     const int kfe = min(kf, kend);
                     const double iwo = iw[o];
                     // w = 1 groups read the pre-summed copies and run the non-interpolating loop
-                    const bool w1 = TM > 4 && uni_rt && wu == 1.0; // (narrow bands: measured slower)
+                    const bool w1 = uni_rt && wu == 1.0;
                     const double2 *gi = (w1 ? F.stages1 : F.stages) + static_cast<size_t>(F.item_base[p] + X) * NB * KS * 32;
                     const double2 *ga = gi + static_cast<size_t>(b) * KS * 32 + lane;
                     const int g0 = __ldg(F.grange + 2 * vb), g1 = __ldg(F.grange + 2 * vb + 1);
@@ -617,119 +581,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                 bw[nt] = uni ? 0.0 : wq[nt] * bv[nt];
                             }
                         };
-                        if constexpr (TM <= 4) {
-                        // Narrow bands (66 bins): short K-loops whose per-step overhead dominates,
-                        // so the gathers ride in the owner loop (ks-outer, one B load per K-step,
-                        // TM sums live) with the gather weights (pair-independent, L1-resident) and
-                        // the shifted A rows (neighbouring fragments of the same pass) loaded per
-                        // entry; measured faster than the pre-weighted streaming form at this width.
-                        double Z[TM][NT][2];
-#pragma unroll
-                        for (int t = 0; t < TM; ++t)
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) Z[t][nt][0] = Z[t][nt][1] = 0.0;
-                        const int kgl = skg[2 * vb], kgh = skg[2 * vb + 1];
-                        auto far_step = [&](int ks, double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
-                            const double c0 = fma(-xs[4 * ks + lc], iwo, 1.0); // 1 - x_s / width_o
-                            const double a2 = a * c0, ad2 = ad * c0;
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) {
-                                dmma(Xf[nt][0], Xf[nt][1], a, bv[nt]);
-                                dmma(Yf[nt][0], Yf[nt][1], a2, bv[nt]);
-                                if (!uni) {
-                                    dmma(Xf[nt][0], Xf[nt][1], ad, bw[nt]);
-                                    dmma(Yf[nt][0], Yf[nt][1], ad2, bw[nt]);
-                                }
-                            }
-                        };
-                        auto loss_step = [&](double a, double ad, const double (&bv)[NT], const double (&bw)[NT]) {
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) {
-                                dmma(L[nt][0], L[nt][1], a, bv[nt]);
-                                if (!uni) dmma(L[nt][0], L[nt][1], ad, bw[nt]);
-                            }
-                        };
-                        int ks = 0;
-                        // (1) far steps before any gather entry
-#pragma unroll 4
-                        for (; ks < min(kend, min(kf, kgl)); ++ks) {
-                            const double2 kk = __ldg(ga + ks * 32);
-                            double bv[NT], bw[NT];
-                            loadb(ks, bv, bw);
-                            far_step(ks, uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, kk.y, bv, bw);
-                        }
-                        // (2) steps holding gather entries (far or loss + the entries' DMMAs); the
-                        // gather operands are loaded first, the next A fragment one step ahead
-                        {
-                            const int k2end = min(kend, max(kf, kgh));
-                            double2 kkn = ks < k2end ? __ldg(ga + ks * 32) : double2{0.0, 0.0};
-                            auto step2 = [&](int ks, auto FC) {
-                                constexpr bool FAR = decltype(FC)::value;
-                                const double2 kk = kkn;
-                                if (ks + 1 < k2end) kkn = __ldg(ga + (ks + 1) * 32);
-                                const unsigned gmk = sbm[vb * KS + ks];
-                                const int go = sgoff[vb * KS + ks];
-                                double cpre[TM];
-                                double2 kpre[TM];
-                                {
-                                    const double *gc = F.gcoef + static_cast<size_t>(go) * 32 + lane;
-                                    int rk = 0;
-#pragma unroll
-                                    for (int t = 0; t < TM; ++t) {
-                                        const bool ont = gmk >> t & 1u;
-                                        cpre[t] = ont ? __ldg(gc + 32 * rk) : 0.0;
-                                        rk += ont ? 1 : 0;
-                                        const int ot = max(o - t, 0); // rows < 0 carry c == 0
-                                        kpre[t] = ont && t > 0 ? __ldg(gi + (static_cast<size_t>(ot >> 3) * KS + ks) * 32 +
-                                                                       (((ot & 7) << 2) | lc))
-                                                               : double2{0.0, 0.0};
-                                    }
-                                }
-                                double bv[NT], bw[NT];
-                                loadb(ks, bv, bw);
-                                const double a = uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, ad = kk.y;
-                                if constexpr (FAR) far_step(ks, a, ad, bv, bw);
-                                else loss_step(a, ad, bv, bw);
-                                if (gmk) {
-#pragma unroll
-                                    for (int t = 0; t < TM; ++t) {
-                                        if (gmk >> t & 1u) {
-                                            const double at = t > 0 ? (uni ? (w0 ? kpre[t].x : fma(wu, kpre[t].y, kpre[t].x)) : kpre[t].x) : a;
-                                            const double adt = t > 0 ? kpre[t].y : ad;
-                                            const double a2 = at * cpre[t], ad2 = adt * cpre[t];
-#pragma unroll
-                                            for (int nt = 0; nt < NT; ++nt) {
-                                                dmma(Z[t][nt][0], Z[t][nt][1], a2, bv[nt]);
-                                                if (!uni) dmma(Z[t][nt][0], Z[t][nt][1], ad2, bw[nt]);
-                                            }
-                                        }
-                                    }
-                                }
-                            };
-                            for (; ks < min(k2end, kf); ++ks) step2(ks, std::true_type{});
-                            for (; ks < k2end; ++ks) step2(ks, std::false_type{});
-                        }
-                        // (3) loss-only steps above the band
-#pragma unroll 4
-                        for (; ks < kend; ++ks) {
-                            const double2 kk = __ldg(ga + ks * 32);
-                            double bv[NT], bw[NT];
-                            loadb(ks, bv, bw);
-                            loss_step(uni ? (w0 ? kk.x : fma(wu, kk.y, kk.x)) : kk.x, kk.y, bv, bw);
-                        }
-#pragma unroll
-                        for (int t = 0; t < TM; ++t) { // the band sums, scaled by the owner value f(o-t)
-                            const int ot = o - t;
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                                for (int e2 = 0; e2 < 2; ++e2) {
-                                    const int q = qg + 8 * nt + 2 * lc + e2;
-                                    const double ft = on[nt][e2] && ot >= 0 ? W(fcat, ot, q) : 0.0;
-                                    hz[nt][e2] = fma(ft, Z[t][nt][e2], hz[nt][e2]);
-                                }
-                        }
-                        } else {
                         // (A) the owner block's K-steps: far [0, kfe) (X/Y identity), loss [kfe, kend).
                         // A fragments stream from L2 in chunks of DA; the next chunk is in flight
                         // during this one's DMMAs (tables padded: no bounds checks on the loads).
@@ -857,7 +708,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1) coal_dmmag_kernel(StepArgs A, Dm
                                     tk[j] = tkn[j];
                                 }
                             }
-                        }
                         }
                     };
                     if (!uni_rt) kloop(std::integral_constant<int, 0>{});
@@ -1010,8 +860,7 @@ inline size_t dmmag_smem_bytes(const DmmagTables &T, int NP, bool lean, bool pad
     size_t b = (static_cast<size_t>(kNCat) * T.SR * (NP + (pad ? 4 : 0)) + 2 * (T.SR + 8) + NP) * sizeof(double) + NP * 24 +
                3 * T.nblk * 4 + MP * 4 + 4 * (MP + 1) * 4 + static_cast<size_t>(NP / 16) * T.nblk * 4 +
                MP * T.nblk * 2 + 16;
-    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double) +
-                    (T.TM <= 4 ? 3 * static_cast<size_t>(T.nblk) * T.KS * 6 + 6 * T.nblk * 4 : 0);
+    if (!lean) b += static_cast<size_t>(kNCat) * T.nblk * NP * sizeof(double);
     return b;
 }
 
@@ -1055,10 +904,6 @@ inline int launch_dmmag_t(const DmmagTables &T, const StepArgs &A, int num_sms, 
     F.bstages1 = T.bstages1;
     F.gtk = T.gtk;
     F.grange = T.grange;
-    F.bmask = T.bmask;
-    F.goff = T.goff;
-    F.kg = T.kg;
-    F.gcoef = T.gcoef;
     for (int i = 0; i < 2 * kMaxPairs; ++i) F.bofs[i] = T.bofs[i];
     if (NKRC && NKRC != T.nkr) return -1;
     auto kern = coal_dmmag_kernel<TM, G, MAXW, PAD, NKRC>;
